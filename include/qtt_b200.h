@@ -1,0 +1,154 @@
+/*
+ * qtt_b200.h — C ABI of the B200-native QTT hot path (libqttb200.so).
+ *
+ * Drop-in boundary for the tensor-train linear algebra of the reference
+ * package `qttfem` (arXiv 2501.07778).  The reference is pure Python over
+ * numpy/LAPACK, so its "FFI" for this path is the set of module functions
+ * listed next to every entry point below; the Python mirror
+ * (paper_2501_07778_b200/*.py) binds these symbols with ctypes and keeps the
+ * reference signatures, argument meanings and ValueError/TypeError behaviour.
+ *
+ * Conventions
+ *   - All numeric buffers are device pointers to FP64 data.
+ *   - A TT object is a packed buffer of cores plus a host-side qtt_layout:
+ *     vector cores (r_l, n_l, r_{l+1}) and matrix cores (r_l, n_l, m_l,
+ *     r_{l+1}), C-contiguous, exactly the reference core layouts
+ *     (ttcore.py:55-138); core l starts at data + offsets[l] (element offset,
+ *     multiple of 32 so every core is 256-byte aligned).
+ *   - Mode 1 is the least significant index bit (ttcore.py:3-10).
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).
+ *   - Return value: QTT_OK or one of the QTT_E* codes.  Entry points that
+ *     return data-dependent ranks write them into the caller's out layout;
+ *     they synchronise `stream` once to do so.
+ *   - The caller owns every output buffer.  Temporary device memory comes
+ *     from the CUDA stream-ordered allocator on `stream`.
+ */
+#ifndef QTT_B200_H_
+#define QTT_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QTT_MAX_CORES 64
+
+enum {
+  QTT_OK = 0,
+  QTT_EINVAL = 1,      /* shape / argument error (Python raises ValueError) */
+  QTT_ECUDA = 2,       /* CUDA runtime error                               */
+  QTT_EWORKSPACE = 3,  /* output buffer too small                          */
+  QTT_EUNSUPPORTED = 4 /* size outside the kernels' envelope              */
+};
+
+typedef struct qtt_layout {
+  int32_t d;                         /* number of cores                     */
+  int32_t is_matrix;                 /* 0: vector cores, 1: matrix cores    */
+  int64_t ranks[QTT_MAX_CORES + 1];  /* r_0 .. r_d (r_0 = r_d = 1)          */
+  int64_t rows[QTT_MAX_CORES];       /* n_l                                 */
+  int64_t cols[QTT_MAX_CORES];       /* m_l (1 for vectors)                 */
+  int64_t offsets[QTT_MAX_CORES];    /* element offset of core l            */
+} qtt_layout;
+
+/* Library identification; returns a static string. */
+const char* qtt_version(void);
+
+/* Number of doubles a packed buffer for `lay` needs (with alignment). */
+int64_t qtt_layout_size(const qtt_layout* lay);
+
+/* ---------------------------------------------------------------- (a2,a3)
+ * Exact core-wise products, all cores in ONE launch.
+ * qtt_matvec  replaces ttcore.tt_matvec  (ttcore.py:443-455):
+ *   y_l[(a,c), i, (b,e)] = sum_j A_l[a,i,j,b] x_l[c,j,e]
+ * qtt_matmat  replaces ttcore.tt_matmat  (ttcore.py:458-470).
+ * qtt_hadamard replaces ttcore.tt_hadamard (ttcore.py:421-440); for matrix
+ *   operands the modes are the merged (i,j) pairs.
+ * Output layouts (ranks = products) are computed by the caller. */
+int qtt_matvec(const qtt_layout* A, const double* a, const qtt_layout* x,
+               const double* xd, const qtt_layout* y, double* yd, void* stream);
+int qtt_matmat(const qtt_layout* A, const double* a, const qtt_layout* B,
+               const double* b, const qtt_layout* C, double* c, void* stream);
+int qtt_hadamard(const qtt_layout* A, const double* a, const qtt_layout* B,
+                 const double* b, const qtt_layout* C, double* c, void* stream);
+
+/* ------------------------------------------------------------------- (a4)
+ * Structural algebra, one launch each.
+ * qtt_add      replaces tt_add      (ttcore.py:380-411), scales b by beta.
+ * qtt_zkron    replaces tt_zkron    (ttcore.py:501-539).
+ * qtt_diag     replaces tt_diag     (ttcore.py:478-486).
+ * qtt_transpose replaces tt_transpose (ttcore.py:473-475).
+ * qtt_scale    replaces tt_scale    (ttcore.py:414-418): copy, core 0 * s. */
+int qtt_add(const qtt_layout* A, const double* a, const qtt_layout* B,
+            const double* b, double beta, const qtt_layout* C, double* c,
+            void* stream);
+int qtt_zkron(const qtt_layout* A, const double* a, const qtt_layout* B,
+              const double* b, const qtt_layout* C, double* c, void* stream);
+int qtt_diag(const qtt_layout* V, const double* v, const qtt_layout* D,
+             double* dd, void* stream);
+int qtt_transpose(const qtt_layout* A, const double* a, const qtt_layout* T,
+                  double* t, void* stream);
+int qtt_scale(const qtt_layout* A, const double* a, double s, double* out,
+              void* stream);
+
+/* ------------------------------------------------------------------- (a5)
+ * TT rounding, replaces ttcore.tt_round (ttcore.py:322-338):
+ * right-to-left Householder QR sweep, then left-to-right truncated SVD sweep
+ * with delta = eps/sqrt(d-1)*||t|| and the _chop rule (ttcore.py:175-190).
+ * `out` receives the final ranks/offsets; out_data needs
+ * qtt_layout_size(in) doubles (ranks never increase). */
+int qtt_round(const qtt_layout* in, const double* in_data, double eps,
+              qtt_layout* out, double* out_data, void* stream);
+
+/* ------------------------------------------------------------------- (a6)
+ * TT-SVD of a dense vector, replaces ttcore.tt_decompose for 1-D input
+ * (ttcore.py:211-235, _tt_svd 193-208).  `sizes` are the d mode sizes;
+ * `dense` is read only.  `out` receives ranks/offsets; out_data must hold
+ * `out_capacity` doubles. */
+int qtt_decompose(const double* dense, int32_t d, const int64_t* sizes,
+                  double eps, qtt_layout* out, double* out_data,
+                  int64_t out_capacity, void* stream);
+
+/* ------------------------------------------------------------------- (a7)
+ * Norm / inner product (ttcore.py:341-363); results land in host memory. */
+int qtt_norm(const qtt_layout* A, const double* a, double* result,
+             void* stream);
+int qtt_dot(const qtt_layout* A, const double* a, const qtt_layout* B,
+            const double* b, double* result, void* stream);
+
+/* ------------------------------------------------------------- (a8,a14)
+ * Dense realisation (ttcore.tt_contract, ttcore.py:267-293) and dense
+ * operator application (solver.apply_tt_matrix, solver.py:57-78). */
+int qtt_contract(const qtt_layout* A, const double* a, double* dense,
+                 void* stream);
+int qtt_dense_apply(const qtt_layout* A, const double* a, const double* v,
+                    double* out, void* stream);
+
+/* ------------------------------------------------------------------- (a9)
+ * Index maps, bit exact (indexing.py:58-112).  perm has 4^d (node) or
+ * 2*4^d (dof) int64 entries on the device. */
+int qtt_zorder_permutation(int32_t d, int64_t* perm, void* stream);
+int qtt_zorder_dof_permutation(int32_t d, int64_t* perm, void* stream);
+int qtt_z_index(int32_t d, int64_t count, const int64_t* i, const int64_t* j,
+                int64_t* z, void* stream);
+
+/* ------------------------------------------------------ dense primitives
+ * Exposed for the parity tests of the building blocks. */
+int qtt_gemm(int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,
+             int64_t k, double alpha, const double* a, int64_t lda,
+             const double* b, int64_t ldb, double beta, double* c,
+             int64_t ldc, void* stream);
+/* Householder QR of a column-major m x n matrix: Q (m x k), R (k x n). */
+int qtt_qr(int64_t m, int64_t n, const double* a, int64_t lda, double* q,
+           int64_t ldq, double* r, int64_t ldr, void* stream);
+/* Singular values (descending) and left singular vectors (u, m x min(m,n))
+ * of a column-major m x n matrix via QR + one-sided Jacobi. */
+int qtt_svd(int64_t m, int64_t n, const double* a, int64_t lda, double* s,
+            double* u, int64_t ldu, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QTT_B200_H_ */

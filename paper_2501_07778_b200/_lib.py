@@ -1,0 +1,125 @@
+"""ctypes binding of ``libqttb200.so`` (the C ABI in include/qtt_b200.h).
+
+There is no CPU fallback: importing works without a GPU (so the host-side
+modules and the symbol table can be inspected), but every compute entry
+point raises when the shared library or a CUDA device is missing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+MAX_CORES = 64
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libqttb200.so")
+
+QTT_OK, QTT_EINVAL, QTT_ECUDA, QTT_EWORKSPACE, QTT_EUNSUPPORTED = range(5)
+
+# Every symbol declared in include/qtt_b200.h (checked by tests/test_abi.py).
+EXPORTS = (
+    "qtt_version",
+    "qtt_layout_size",
+    "qtt_matvec",
+    "qtt_matmat",
+    "qtt_hadamard",
+    "qtt_add",
+    "qtt_zkron",
+    "qtt_diag",
+    "qtt_transpose",
+    "qtt_scale",
+    "qtt_round",
+    "qtt_decompose",
+    "qtt_norm",
+    "qtt_dot",
+    "qtt_contract",
+    "qtt_dense_apply",
+    "qtt_zorder_permutation",
+    "qtt_zorder_dof_permutation",
+    "qtt_z_index",
+    "qtt_gemm",
+    "qtt_qr",
+    "qtt_svd",
+)
+
+
+class Layout(ctypes.Structure):
+    """Mirror of ``qtt_layout``."""
+
+    _fields_ = [
+        ("d", ctypes.c_int32),
+        ("is_matrix", ctypes.c_int32),
+        ("ranks", ctypes.c_int64 * (MAX_CORES + 1)),
+        ("rows", ctypes.c_int64 * MAX_CORES),
+        ("cols", ctypes.c_int64 * MAX_CORES),
+        ("offsets", ctypes.c_int64 * MAX_CORES),
+    ]
+
+
+class QTTError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def load():
+    """Load the shared library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise QTTError(
+                f"libqttb200.so not built ({_LIB_PATH}); run `make` or "
+                "`python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        lib = ctypes.CDLL(_LIB_PATH)
+        lib.qtt_version.restype = ctypes.c_char_p
+        lib.qtt_layout_size.restype = ctypes.c_int64
+        for name in EXPORTS:
+            if name not in ("qtt_version", "qtt_layout_size"):
+                getattr(lib, name).restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise QTTError("paper_2501_07778_b200 needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle() -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t: torch.Tensor | None) -> ctypes.c_void_p:
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def check(status: int, what: str) -> None:
+    if status == QTT_OK:
+        return
+    names = {
+        QTT_EINVAL: "invalid argument",
+        QTT_ECUDA: "CUDA error",
+        QTT_EWORKSPACE: "output buffer too small",
+        QTT_EUNSUPPORTED: "size outside the kernel envelope",
+    }
+    msg = f"{what}: {names.get(status, status)}"
+    if status == QTT_EINVAL:
+        raise ValueError(msg)
+    raise QTTError(msg)
+
+
+def call(name: str, *args) -> None:
+    lib = load()
+    check(getattr(lib, name)(*args), name)
+
+
+def align(n: int) -> int:
+    return (n + 31) // 32 * 32

@@ -1,0 +1,98 @@
+// Shared helpers for the B200 QTT kernels (sm_100a, FP64 throughout).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <algorithm>
+
+namespace qtt {
+
+// Status codes returned by every C-ABI entry point (include/qtt_b200.h).
+enum Status : int {
+  kOk = 0,
+  kInvalid = 1,
+  kCuda = 2,
+  kWorkspace = 3,
+  kUnsupported = 4,
+};
+
+constexpr int kMaxCores = 96;  // QTT depth supported by by-value descriptors
+
+#define QTT_CUDA(expr)                                                     \
+  do {                                                                     \
+    cudaError_t _e = (expr);                                               \
+    if (_e != cudaSuccess) {                                               \
+      fprintf(stderr, "[qtt_b200] CUDA error %s at %s:%d: %s\n",           \
+              cudaGetErrorName(_e), __FILE__, __LINE__,                    \
+              cudaGetErrorString(_e));                                     \
+      return ::qtt::kCuda;                                                 \
+    }                                                                      \
+  } while (0)
+
+#define QTT_CHECK_LAUNCH() QTT_CUDA(cudaGetLastError())
+
+#define QTT_TRY(expr)                    \
+  do {                                   \
+    int _s = (expr);                     \
+    if (_s != ::qtt::kOk) return _s;     \
+  } while (0)
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) {
+  return (a + b - 1) / b;
+}
+
+inline int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ------------------------------------------------------------------ GEMM
+// Column-major FP64 GEMM on the DMMA (mma.sync m8n8k4 f64) tensor pipe:
+//   C[b] = alpha * op(A[b]) * op(B[b]) + beta * C[b]
+// op(X) = X or X^T.  Batched through strides (0 stride = shared operand).
+struct GemmArgs {
+  int m, n, k;
+  int trans_a, trans_b;
+  double alpha, beta;
+  const double* a;
+  int64_t lda, stride_a;
+  const double* b;
+  int64_t ldb, stride_b;
+  double* c;
+  int64_t ldc, stride_c;
+  int batch;
+};
+
+int gemm(const GemmArgs& g, cudaStream_t stream);
+
+// Convenience: single column-major GEMM.
+inline int dgemm(cudaStream_t s, int ta, int tb, int m, int n, int k, double alpha,
+                 const double* a, int64_t lda, const double* b, int64_t ldb,
+                 double beta, double* c, int64_t ldc) {
+  GemmArgs g{m, n, k, ta, tb, alpha, beta, a, lda, 0, b, ldb, 0, c, ldc, 0, 1};
+  return gemm(g, s);
+}
+
+// Out-of-place transpose of a column-major (rows x cols) matrix into
+// a column-major (cols x rows) matrix.
+int transpose(cudaStream_t s, int rows, int cols, const double* src, int64_t lds,
+              double* dst, int64_t ldd);
+
+int fill(cudaStream_t s, double* p, int64_t n, double v);
+int copy_matrix(cudaStream_t s, int rows, int cols, const double* src, int64_t lds,
+                double* dst, int64_t ldd);
+
+}  // namespace qtt

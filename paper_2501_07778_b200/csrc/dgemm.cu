@@ -1,0 +1,223 @@
+// FP64 GEMM on the DMMA tensor pipe (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4).
+//
+// B200 has no tcgen05 kind for f64: the FP64 tensor path is the DMMA unit
+// fed from registers, so this kernel stages 64x64x16 tiles through shared
+// memory with cp.async double buffering and runs 2x2 warps of 32x32 warp
+// tiles (16 DMMA accumulators per warp).  Column-major operands, optional
+// transposes, strided batching.  Used for every dense contraction of the
+// TT hot path: rounding carries, compact-WY updates, Jacobi rotations,
+// AMEn environment contractions and the dense residual.
+#include "common.cuh"
+
+namespace qtt {
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, PAD = 4, THREADS = 128;
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+template <int TA, int TB>
+__global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt) {
+  __shared__ double As[2][BK][BM + PAD];
+  __shared__ double Bs[2][BK][BN + PAD];
+
+  const int tile = blockIdx.x;
+  const int m0 = (tile % mt) * BM;
+  const int n0 = (tile / mt) * BN;
+  const int bz = blockIdx.y;
+  const double* A = g.a + bz * g.stride_a;
+  const double* B = g.b + bz * g.stride_b;
+  double* C = g.c + bz * g.stride_c;
+  const int M = g.m, N = g.n, K = g.k;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+
+  auto load_tile = [&](int buf, int k0) {
+#pragma unroll
+    for (int e = 0; e < (BM * BK) / THREADS; ++e) {
+      int idx = t + e * THREADS;
+      int mm, kk;
+      if (TA == 0) { mm = idx % BM; kk = idx / BM; } else { kk = idx % BK; mm = idx / BK; }
+      int gm = m0 + mm, gk = k0 + kk;
+      bool ok = gm < M && gk < K;
+      const double* src = ok ? (TA == 0 ? A + gm + (int64_t)gk * g.lda : A + gk + (int64_t)gm * g.lda) : A;
+      cp_async8(&As[buf][kk][mm], src, ok);
+    }
+#pragma unroll
+    for (int e = 0; e < (BN * BK) / THREADS; ++e) {
+      int idx = t + e * THREADS;
+      int nn, kk;
+      if (TB == 0) { kk = idx % BK; nn = idx / BK; } else { nn = idx % BN; kk = idx / BN; }
+      int gn = n0 + nn, gk = k0 + kk;
+      bool ok = gn < N && gk < K;
+      const double* src = ok ? (TB == 0 ? B + gk + (int64_t)gn * g.ldb : B + gn + (int64_t)gk * g.ldb) : B;
+      cp_async8(&Bs[buf][kk][nn], src, ok);
+    }
+    cp_async_commit();
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int ktiles = (K + BK - 1) / BK;
+  if (ktiles > 0) load_tile(0, 0);
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < ktiles) {
+      load_tile(buf ^ 1, (kt + 1) * BK);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 4) {
+      double af[4], bf[4];
+      const int kr = ks + (lane & 3);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[buf][kr][wm + i * 8 + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][kr][wn + j * 8 + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+
+  const double alpha = g.alpha, beta = g.beta;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + wm + i * 8 + (lane >> 2);
+    if (row >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = n0 + wn + j * 8 + 2 * (lane & 3) + h;
+        if (col < N) {
+          double* p = C + row + (int64_t)col * g.ldc;
+          double v = alpha * acc[i][j][h];
+          if (beta != 0.0) v += beta * *p;
+          *p = v;
+        }
+      }
+    }
+  }
+}
+
+__global__ void scale_kernel(GemmArgs g) {
+  // k == 0 (or alpha == 0): C = beta * C
+  int64_t total = (int64_t)g.m * g.n;
+  double* C = g.c + blockIdx.y * g.stride_c;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int r = i % g.m;
+    int64_t c = i / g.m;
+    double* p = C + r + c * g.ldc;
+    *p = g.beta == 0.0 ? 0.0 : g.beta * *p;
+  }
+}
+
+__global__ void transpose_kernel(int rows, int cols, const double* __restrict__ src, int64_t lds,
+                                 double* __restrict__ dst, int64_t ldd) {
+  __shared__ double tile[32][33];
+  int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    int r = r0 + threadIdx.x, c = c0 + j;
+    if (r < rows && c < cols) tile[j][threadIdx.x] = src[r + (int64_t)c * lds];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    int c = c0 + threadIdx.x, r = r0 + j;
+    if (r < rows && c < cols) dst[c + (int64_t)r * ldd] = tile[threadIdx.x][j];
+  }
+}
+
+__global__ void fill_kernel(double* p, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void copy_matrix_kernel(int rows, int cols, const double* __restrict__ src, int64_t lds,
+                                   double* __restrict__ dst, int64_t ldd) {
+  int64_t total = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int r = i % rows;
+    int64_t c = i / rows;
+    dst[r + c * ldd] = src[r + c * lds];
+  }
+}
+
+}  // namespace
+
+int gemm(const GemmArgs& g, cudaStream_t stream) {
+  if (g.m < 0 || g.n < 0 || g.k < 0 || g.batch < 0) return kInvalid;
+  if (g.m == 0 || g.n == 0 || g.batch == 0) return kOk;
+  if (g.batch > 65535) return kUnsupported;
+  if (g.k == 0 || g.alpha == 0.0) {
+    dim3 grid((unsigned)std::min<int64_t>(ceil_div((int64_t)g.m * g.n, 256), 4096), g.batch);
+    scale_kernel<<<grid, 256, 0, stream>>>(g);
+    QTT_CHECK_LAUNCH();
+    return kOk;
+  }
+  const int mt = (int)ceil_div(g.m, BM);
+  const int64_t tiles = (int64_t)mt * ceil_div(g.n, BN);
+  if (tiles > 0x7fffffff) return kUnsupported;
+  dim3 grid((unsigned)tiles, g.batch);
+  if (!g.trans_a && !g.trans_b) gemm_kernel<0, 0><<<grid, THREADS, 0, stream>>>(g, mt);
+  else if (!g.trans_a && g.trans_b) gemm_kernel<0, 1><<<grid, THREADS, 0, stream>>>(g, mt);
+  else if (g.trans_a && !g.trans_b) gemm_kernel<1, 0><<<grid, THREADS, 0, stream>>>(g, mt);
+  else gemm_kernel<1, 1><<<grid, THREADS, 0, stream>>>(g, mt);
+  QTT_CHECK_LAUNCH();
+  return kOk;
+}
+
+int transpose(cudaStream_t s, int rows, int cols, const double* src, int64_t lds, double* dst,
+              int64_t ldd) {
+  if (rows <= 0 || cols <= 0) return kOk;
+  dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(cols, 32));
+  if (grid.y > 65535) return kUnsupported;
+  transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(rows, cols, src, lds, dst, ldd);
+  QTT_CHECK_LAUNCH();
+  return kOk;
+}
+
+int fill(cudaStream_t s, double* p, int64_t n, double v) {
+  if (n <= 0) return kOk;
+  int blocks = (int)std::min<int64_t>(ceil_div(n, 256), 8 * num_sms());
+  fill_kernel<<<blocks, 256, 0, s>>>(p, n, v);
+  QTT_CHECK_LAUNCH();
+  return kOk;
+}
+
+int copy_matrix(cudaStream_t s, int rows, int cols, const double* src, int64_t lds, double* dst,
+                int64_t ldd) {
+  if (rows <= 0 || cols <= 0) return kOk;
+  int blocks = (int)std::min<int64_t>(ceil_div((int64_t)rows * cols, 256), 8 * num_sms());
+  copy_matrix_kernel<<<blocks, 256, 0, s>>>(rows, cols, src, lds, dst, ldd);
+  QTT_CHECK_LAUNCH();
+  return kOk;
+}
+
+}  // namespace qtt

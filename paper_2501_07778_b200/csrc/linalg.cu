@@ -1,0 +1,672 @@
+// Dense FP64 factorizations for the TT sweeps: blocked Householder QR with
+// cluster (DSMEM) panels, one-sided Jacobi SVD, sort + _chop, and the
+// triangular-inverse certificate that skips the SVD when no truncation can
+// occur.  See linalg.cuh for the contracts.
+#include <cooperative_groups.h>
+
+#include "linalg.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace qtt {
+namespace {
+
+constexpr double kEps = 2.220446049250313e-16;
+
+// ------------------------------------------------------------------ panel QR
+constexpr int PNB = 32;          // panel width
+constexpr int PTHREADS = 256;    // 8 warps per CTA
+constexpr int PMAXROWS = 736;    // panel rows held per CTA (736*32*8 B = 184 KB)
+constexpr int PMAXCLUSTER = 16;  // non-portable cluster size (B200: 16 SMs per cluster)
+
+struct PanelArgs {
+  int m, nb, rpc;
+  double* A;
+  int64_t lda;
+  double* V;
+  int64_t ldv;
+  double* Y;
+  int64_t ldy;
+  double* Y2;
+  int64_t ldy2;
+  double* tau;
+};
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  // PTHREADS-thread reduction; returns the total to every thread.
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < PTHREADS / 32; ++w) t += red[w];
+  return t;
+}
+
+__global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
+  extern __shared__ double smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cs = (int)cluster.num_blocks();
+  const int crank = (int)cluster.block_rank();
+  const int ld = pa.rpc;
+  const int row0 = crank * pa.rpc;
+  const int nrows = max(0, min(pa.m - row0, pa.rpc));
+  const int nb = pa.nb;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  double* P = smem;                    // ld * PNB
+  double* partA = P + (size_t)ld * PNB;  // 2
+  double* partB = partA + 2;           // PNB
+  double* gram = partB + PNB;          // PNB*PNB (partial)
+  double* G = gram + PNB * PNB;        // PNB*PNB (total)
+  double* T = G + PNB * PNB;           // PNB*PNB
+  double* red = T + PNB * PNB;         // PTHREADS/32
+  double* tau_s = red + PTHREADS / 32; // PNB
+
+  for (int idx = tid; idx < nrows * nb; idx += PTHREADS) {
+    const int r = idx % nrows, c = idx / nrows;
+    P[r + c * ld] = pa.A[(row0 + r) + (int64_t)c * pa.lda];
+  }
+  __syncthreads();
+
+  for (int j = 0; j < nb; ++j) {
+    // ---- phase A: norm of the sub-diagonal part of column j
+    double sq = 0.0;
+    for (int r = tid; r < nrows; r += PTHREADS) {
+      if (row0 + r > j) {
+        const double x = P[r + j * ld];
+        sq = fma(x, x, sq);
+      }
+    }
+    sq = block_sum(sq, red);
+    if (tid == 0) {
+      partA[0] = sq;
+      partA[1] = (j >= row0 && j < row0 + nrows) ? P[(j - row0) + j * ld] : 0.0;
+    }
+    cluster.sync();
+    double norm2 = 0.0;
+    for (int c = 0; c < cs; ++c) norm2 += cluster.map_shared_rank(partA, c)[0];
+    const int owner = min(j / pa.rpc, cs - 1);
+    const double alpha = cluster.map_shared_rank(partA, owner)[1];
+    double tau = 0.0, beta = alpha, scal = 1.0;
+    if (norm2 > 0.0) {
+      const double nrm = sqrt(fma(alpha, alpha, norm2));
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    for (int r = tid; r < nrows; r += PTHREADS) {
+      const int g = row0 + r;
+      if (g > j) P[r + j * ld] *= scal;
+      else if (g == j) P[r + j * ld] = beta;
+    }
+    if (tid == 0) tau_s[j] = tau;
+    __syncthreads();
+    // ---- phase B: w_c = v^T A[:, c] for the remaining panel columns
+    for (int c = j + 1 + warp; c < nb; c += PTHREADS / 32) {
+      double w = 0.0;
+      for (int r = lane; r < nrows; r += 32) {
+        const int g = row0 + r;
+        if (g >= j) {
+          const double v = (g == j) ? 1.0 : P[r + j * ld];
+          w = fma(v, P[r + c * ld], w);
+        }
+      }
+      w = warp_sum(w);
+      if (lane == 0) partB[c] = w;
+    }
+    cluster.sync();
+    if (tau != 0.0) {
+      for (int c = j + 1; c < nb; ++c) {
+        double w = 0.0;
+        for (int q = 0; q < cs; ++q) w += cluster.map_shared_rank(partB, q)[c];
+        const double tw = tau * w;
+        for (int r = tid; r < nrows; r += PTHREADS) {
+          const int g = row0 + r;
+          if (g >= j) {
+            const double v = (g == j) ? 1.0 : P[r + j * ld];
+            P[r + c * ld] = fma(-tw, v, P[r + c * ld]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- Gram of V for the compact-WY T factor (dlarft, forward, columnwise)
+  for (int pq = tid; pq < nb * nb; pq += PTHREADS) {
+    const int p = pq % nb, q = pq / nb;
+    double acc = 0.0;
+    for (int r = 0; r < nrows; ++r) {
+      const int g = row0 + r;
+      const double vp = (g == p) ? 1.0 : (g > p ? P[r + p * ld] : 0.0);
+      const double vq = (g == q) ? 1.0 : (g > q ? P[r + q * ld] : 0.0);
+      acc = fma(vp, vq, acc);
+    }
+    gram[p + q * PNB] = acc;
+  }
+  cluster.sync();
+  for (int pq = tid; pq < nb * nb; pq += PTHREADS) {
+    const int p = pq % nb, q = pq / nb;
+    double acc = 0.0;
+    for (int c = 0; c < cs; ++c) acc += cluster.map_shared_rank(gram, c)[p + q * PNB];
+    G[p + q * PNB] = acc;
+  }
+  cluster.sync();  // remote gram reads done before any CTA may exit
+  if (warp == 0) {
+    for (int j = 0; j < nb; ++j) {
+      double tij = 0.0;
+      if (lane < j) {
+        for (int l = lane; l < j; ++l) tij = fma(T[lane + l * PNB], G[l + j * PNB], tij);
+        tij *= -tau_s[j];
+      }
+      __syncwarp();
+      if (lane < j) T[lane + j * PNB] = tij;
+      if (lane == j) T[j + j * PNB] = tau_s[j];
+      if (lane > j && lane < nb) T[lane + j * PNB] = 0.0;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+
+  // ---- outputs: V (explicit), Y = V T^T, Y2 = V T, R rows, tau
+  for (int idx = tid; idx < nrows * nb; idx += PTHREADS) {
+    const int r = idx % nrows, q = idx / nrows;
+    const int g = row0 + r;
+    double y = 0.0, y2 = 0.0;
+    for (int p = 0; p < nb; ++p) {
+      const double v = (g == p) ? 1.0 : (g > p ? P[r + p * ld] : 0.0);
+      y = fma(v, T[q + p * PNB], y);
+      y2 = fma(v, T[p + q * PNB], y2);
+    }
+    const double vq = (g == q) ? 1.0 : (g > q ? P[r + q * ld] : 0.0);
+    pa.V[g + (int64_t)q * pa.ldv] = vq;
+    pa.Y[g + (int64_t)q * pa.ldy] = y;
+    pa.Y2[g + (int64_t)q * pa.ldy2] = y2;
+    if (g <= q) pa.A[g + (int64_t)q * pa.lda] = P[r + q * ld];
+  }
+  if (crank == 0 && tid < nb) pa.tau[tid] = tau_s[tid];
+}
+
+size_t panel_smem_bytes(int rpc) {
+  return sizeof(double) * ((size_t)rpc * PNB + 2 + PNB + 3 * PNB * PNB + PTHREADS / 32 + PNB);
+}
+
+int launch_panel(cudaStream_t s, const PanelArgs& pa0) {
+  static bool configured = false;
+  if (!configured) {
+    QTT_CUDA(cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)panel_smem_bytes(PMAXROWS)));
+    QTT_CUDA(cudaFuncSetAttribute(panel_qr_kernel,
+                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+  }
+  PanelArgs pa = pa0;
+  const int cs = (int)ceil_div(pa.m, PMAXROWS);
+  if (cs > PMAXCLUSTER) return kUnsupported;
+  pa.rpc = (int)ceil_div(pa.m, cs);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs, 1, 1);
+  cfg.blockDim = dim3(PTHREADS, 1, 1);
+  cfg.dynamicSmemBytes = panel_smem_bytes(pa.rpc);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  QTT_CUDA(cudaLaunchKernelEx(&cfg, panel_qr_kernel, pa));
+  return kOk;
+}
+
+__global__ void upper_copy_kernel(int k, int n, const double* __restrict__ A, int64_t lda,
+                                  double* __restrict__ R, int64_t ldr) {
+  const int64_t total = (int64_t)k * n;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i % k);
+    const int64_t c = i / k;
+    R[r + c * ldr] = (r <= c) ? A[r + c * lda] : 0.0;
+  }
+}
+
+__global__ void identity_kernel(int rows, int cols, double* A, int64_t lda) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i % rows);
+    const int64_t c = i / rows;
+    A[r + c * lda] = (r == c) ? 1.0 : 0.0;
+  }
+}
+
+inline int grid_for(int64_t n, int threads = 256) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), 16 * num_sms()));
+}
+
+// ------------------------------------------------------------------- Jacobi
+// Round-robin (circle method) pair of round r: positions of the list
+// [0, 1 + (r mod kp-1), ...] paired first-with-last.
+__device__ __forceinline__ void rr_pair(int kp, int r, int q, int& i, int& j) {
+  const int m = kp - 1;
+  auto at = [&](int pos) { return pos == 0 ? 0 : 1 + ((pos - 1 + r) % m); };
+  i = at(q);
+  j = at(kp - 1 - q);
+  if (i > j) { int t = i; i = j; j = t; }
+}
+
+// One Jacobi rotation on columns (i, j) by one warp; returns 1 if rotated.
+__device__ int jacobi_pair(double* X, int64_t ldx, double* W, int64_t ldw, int p, int k, int i,
+                           int j, double tol) {
+  const int lane = threadIdx.x & 31;
+  double a = 0.0, b = 0.0, g = 0.0;
+  double* xi = X + (int64_t)i * ldx;
+  double* xj = X + (int64_t)j * ldx;
+  for (int r = lane; r < p; r += 32) {
+    const double u = xi[r], v = xj[r];
+    a = fma(u, u, a);
+    b = fma(v, v, b);
+    g = fma(u, v, g);
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
+  g = warp_sum(g);
+  if (g == 0.0 || !(fabs(g) > tol * sqrt(a) * sqrt(b))) return 0;
+  const double zeta = (b - a) / (2.0 * g);
+  const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+  const double c = 1.0 / sqrt(fma(t, t, 1.0));
+  const double sn = c * t;
+  for (int r = lane; r < p; r += 32) {
+    const double u = xi[r], v = xj[r];
+    xi[r] = c * u - sn * v;
+    xj[r] = sn * u + c * v;
+  }
+  double* wi = W + (int64_t)i * ldw;
+  double* wj = W + (int64_t)j * ldw;
+  for (int r = lane; r < k; r += 32) {
+    const double u = wi[r], v = wj[r];
+    wi[r] = c * u - sn * v;
+    wj[r] = sn * u + c * v;
+  }
+  return 1;
+}
+
+constexpr int JMAXSWEEPS = 60;
+constexpr int JTHREADS = 1024;
+
+// Small problems: one CTA, X and W staged in shared memory.
+__global__ void __launch_bounds__(JTHREADS) jacobi_smem_kernel(int p, int k, double* X,
+                                                                int64_t ldx, double* W,
+                                                                int64_t ldw, double tol) {
+  extern __shared__ double sm[];
+  __shared__ int rotated;
+  double* Xs = sm;
+  double* Ws = sm + (size_t)p * k;
+  for (int idx = threadIdx.x; idx < p * k; idx += blockDim.x)
+    Xs[idx] = X[(idx % p) + (int64_t)(idx / p) * ldx];
+  for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x)
+    Ws[idx] = ((idx % k) == (idx / k)) ? 1.0 : 0.0;
+  const int kp = k + (k & 1);
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int sweep = 0; sweep < JMAXSWEEPS; ++sweep) {
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    int any = 0;
+    for (int r = 0; r < kp - 1; ++r) {
+      for (int q = warp; q < kp / 2; q += nw) {
+        int i, j;
+        rr_pair(kp, r, q, i, j);
+        if (j < k) any |= jacobi_pair(Xs, p, Ws, k, p, k, i, j, tol);
+      }
+      __syncthreads();
+    }
+    if (any && (threadIdx.x & 31) == 0) rotated = 1;
+    __syncthreads();
+    if (!rotated) break;
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < p * k; idx += blockDim.x)
+    X[(idx % p) + (int64_t)(idx / p) * ldx] = Xs[idx];
+  for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x)
+    W[(idx % k) + (int64_t)(idx / k) * ldw] = Ws[idx];
+}
+
+// Large problems: cooperative grid, columns stay in global memory (L2).
+__global__ void __launch_bounds__(256) jacobi_grid_kernel(int p, int k, double* X, int64_t ldx,
+                                                          double* W, int64_t ldw, double tol,
+                                                          int* flags) {
+  cg::grid_group grid = cg::this_grid();
+  const int kp = k + (k & 1);
+  const int gw = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)((gridDim.x * (int64_t)blockDim.x) >> 5);
+  for (int sweep = 0; sweep < JMAXSWEEPS; ++sweep) {
+    int any = 0;
+    for (int r = 0; r < kp - 1; ++r) {
+      for (int q = gw; q < kp / 2; q += nw) {
+        int i, j;
+        rr_pair(kp, r, q, i, j);
+        if (j < k) any |= jacobi_pair(X, ldx, W, ldw, p, k, i, j, tol);
+      }
+      grid.sync();
+    }
+    if (any && (threadIdx.x & 31) == 0) atomicOr(&flags[sweep], 1);
+    grid.sync();
+    if (flags[sweep] == 0) break;
+  }
+}
+
+// --------------------------------------------------------------- sort/chop
+constexpr int SORT_MAX = 8192;
+
+__global__ void __launch_bounds__(1024) sort_chop_kernel(int p, int k, const double* X,
+                                                         int64_t ldx, double* sigma, int* perm,
+                                                         const double* delta_dev,
+                                                         double delta_scale, int rmax,
+                                                         int floor_rule, int* rank_dev) {
+  extern __shared__ double sort_sm[];
+  double* sv = sort_sm;
+  double* ss = sort_sm + k;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c = warp; c < k; c += nw) {
+    double a = 0.0;
+    for (int r = lane; r < p; r += 32) {
+      const double x = X[r + (int64_t)c * ldx];
+      a = fma(x, x, a);
+    }
+    a = warp_sum(a);
+    if (lane == 0) sv[c] = sqrt(a);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    const double v = sv[i];
+    int pos = 0;
+    for (int j = 0; j < k; ++j) {
+      const double w = sv[j];
+      pos += (w > v) || (w == v && j < i);
+    }
+    ss[pos] = v;
+    perm[pos] = i;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) sigma[i] = ss[i];
+  if (threadIdx.x == 0) {
+    double delta = delta_dev ? (*delta_dev) * delta_scale : 0.0;
+    if (floor_rule) delta = fmax(delta, ss[0] * (double)max(k, 2) * kEps);
+    double acc = 0.0;
+    int r = 1;
+    for (int i = k - 1; i >= 0; --i) {
+      acc += ss[i] * ss[i];
+      if (sqrt(acc) > delta) { r = i + 1; break; }
+    }
+    *rank_dev = max(1, min(r, rmax));
+  }
+}
+
+// ----------------------------------------------------------- certificate
+constexpr int TRB = 64;
+
+// Invert the 64x64 diagonal blocks of an upper-triangular R (one CTA each).
+__global__ void trinv_diag_kernel(int k, const double* __restrict__ R, int64_t ldr,
+                                  double* __restrict__ X, int64_t ldx) {
+  extern __shared__ double tri_sm[];
+  double (*Rs)[TRB + 1] = reinterpret_cast<double (*)[TRB + 1]>(tri_sm);
+  double (*Xs)[TRB + 1] = reinterpret_cast<double (*)[TRB + 1]>(tri_sm + TRB * (TRB + 1));
+  const int b0 = blockIdx.x * TRB;
+  const int nb = min(TRB, k - b0);
+  for (int idx = threadIdx.x; idx < TRB * TRB; idx += blockDim.x) {
+    const int r = idx % TRB, c = idx / TRB;
+    Rs[r][c] = (r < nb && c < nb) ? R[(b0 + r) + (int64_t)(b0 + c) * ldr] : 0.0;
+    Xs[r][c] = 0.0;
+  }
+  __syncthreads();
+  const int c = threadIdx.x;
+  if (c < nb) {
+    Xs[c][c] = 1.0 / Rs[c][c];
+    for (int i = c - 1; i >= 0; --i) {
+      double acc = 0.0;
+      for (int l = i + 1; l <= c; ++l) acc = fma(Rs[i][l], Xs[l][c], acc);
+      Xs[i][c] = -acc / Rs[i][i];
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
+    const int r = idx % nb, cc = idx / nb;
+    X[(b0 + r) + (int64_t)(b0 + cc) * ldx] = Xs[r][cc];
+  }
+}
+
+// Deterministic two-stage sum of squares.
+__global__ void sumsq_partial_kernel(int64_t n, const double* __restrict__ x,
+                                     double* __restrict__ part) {
+  __shared__ double red[32];
+  double a = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[i];
+    a = fma(v, v, a);
+  }
+  a = warp_sum(a);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
+  }
+}
+
+__global__ void sum_final_kernel(int nparts, const double* __restrict__ part, double* out,
+                                 int take_sqrt) {
+  __shared__ double red[32];
+  double a = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) a += part[i];
+  a = warp_sum(a);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) *out = take_sqrt ? sqrt(v) : v;
+  }
+}
+
+__global__ void certificate_kernel(int k, const double* rnorm, const double* xnorm,
+                                   const double* delta_dev, double delta_scale, int* ok) {
+  const double rn = *rnorm, xn = *xnorm;
+  const double delta = delta_dev ? (*delta_dev) * delta_scale : 0.0;
+  const double thr = fmax(delta, rn * (double)max(k, 2) * kEps);
+  const bool good = isfinite(xn) && xn > 0.0 && (1.0 / xn) > 1.25 * thr;
+  *ok = good ? 1 : 0;
+}
+
+__global__ void gather_columns_kernel(int rows, int cols, const double* __restrict__ src,
+                                      int64_t lds, const int* __restrict__ perm,
+                                      double* __restrict__ dst, int64_t ldd) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i % rows);
+    const int64_t c = i / rows;
+    dst[r + c * ldd] = src[r + (int64_t)perm[c] * lds];
+  }
+}
+
+}  // namespace
+
+int set_identity(cudaStream_t s, int rows, int cols, double* A, int64_t lda) {
+  if (rows <= 0 || cols <= 0) return kOk;
+  identity_kernel<<<grid_for((int64_t)rows * cols), 256, 0, s>>>(rows, cols, A, lda);
+  QTT_CHECK_LAUNCH();
+  return kOk;
+}
+
+int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
+       double* R, int64_t ldr) {
+  if (m <= 0 || n <= 0) return kInvalid;
+  const int k = std::min(m, n);
+  if (ceil_div(m, PMAXROWS) > PMAXCLUSTER) return kUnsupported;
+  double *Ac, *V, *Y, *Y2, *tau, *W;
+  const int64_t mm = m;
+  QTT_CUDA(cudaMallocAsync(&Ac, sizeof(double) * mm * n, s));
+  QTT_CUDA(cudaMallocAsync(&V, sizeof(double) * mm * k, s));
+  QTT_CUDA(cudaMallocAsync(&Y, sizeof(double) * mm * PNB, s));
+  QTT_CUDA(cudaMallocAsync(&Y2, sizeof(double) * mm * k, s));
+  QTT_CUDA(cudaMallocAsync(&tau, sizeof(double) * (k + 1), s));
+  QTT_CUDA(cudaMallocAsync(&W, sizeof(double) * PNB * (int64_t)std::max(n, k), s));
+  QTT_TRY(copy_matrix(s, m, n, A, lda, Ac, m));
+  for (int j0 = 0; j0 < k; j0 += PNB) {
+    const int nb = std::min(PNB, k - j0);
+    const int mp = m - j0;
+    PanelArgs pa{mp, nb, 0, Ac + j0 + (int64_t)j0 * m, mm, V + j0 + (int64_t)j0 * m, mm,
+                 Y + j0, mm, Y2 + j0 + (int64_t)j0 * m, mm, tau + j0};
+    QTT_TRY(launch_panel(s, pa));
+    const int nt = n - j0 - nb;
+    if (nt > 0) {
+      double* At = Ac + j0 + (int64_t)(j0 + nb) * m;
+      QTT_TRY(dgemm(s, 1, 0, nb, nt, mp, 1.0, V + j0 + (int64_t)j0 * m, mm, At, mm, 0.0, W, nb));
+      QTT_TRY(dgemm(s, 0, 0, mp, nt, nb, -1.0, Y + j0, mm, W, nb, 1.0, At, mm));
+    }
+  }
+  if (R) {
+    upper_copy_kernel<<<grid_for((int64_t)k * n), 256, 0, s>>>(k, n, Ac, mm, R, ldr);
+    QTT_CHECK_LAUNCH();
+  }
+  if (Q) {
+    QTT_TRY(set_identity(s, m, k, Q, ldq));
+    const int last = ((k - 1) / PNB) * PNB;
+    for (int j0 = last; j0 >= 0; j0 -= PNB) {
+      const int nb = std::min(PNB, k - j0);
+      const int mp = m - j0, kc = k - j0;
+      double* Qs = Q + j0 + (int64_t)j0 * ldq;
+      QTT_TRY(dgemm(s, 1, 0, nb, kc, mp, 1.0, V + j0 + (int64_t)j0 * m, mm, Qs, ldq, 0.0, W, nb));
+      QTT_TRY(dgemm(s, 0, 0, mp, kc, nb, -1.0, Y2 + j0 + (int64_t)j0 * m, mm, W, nb, 1.0, Qs, ldq));
+    }
+  }
+  QTT_CUDA(cudaFreeAsync(Ac, s));
+  QTT_CUDA(cudaFreeAsync(V, s));
+  QTT_CUDA(cudaFreeAsync(Y, s));
+  QTT_CUDA(cudaFreeAsync(Y2, s));
+  QTT_CUDA(cudaFreeAsync(tau, s));
+  QTT_CUDA(cudaFreeAsync(W, s));
+  return kOk;
+}
+
+int jacobi(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw) {
+  if (p <= 0 || k <= 0) return kInvalid;
+  const double tol = sqrt((double)std::max(p, 1)) * kEps;
+  const size_t smem = sizeof(double) * ((size_t)p * k + (size_t)k * k);
+  if (smem <= 200 * 1024) {
+    static bool configured = false;
+    if (!configured) {
+      QTT_CUDA(cudaFuncSetAttribute(jacobi_smem_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      configured = true;
+    }
+    const int threads = std::min(JTHREADS, std::max(32, ((k + 1) / 2) * 32));
+    jacobi_smem_kernel<<<1, threads, smem, s>>>(p, k, X, ldx, W, ldw, tol);
+    QTT_CHECK_LAUNCH();
+    return kOk;
+  }
+  QTT_TRY(set_identity(s, k, k, W, ldw));
+  int* flags;
+  QTT_CUDA(cudaMallocAsync(&flags, sizeof(int) * JMAXSWEEPS, s));
+  QTT_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * JMAXSWEEPS, s));
+  int dev = 0, per_sm = 0;
+  QTT_CUDA(cudaGetDevice(&dev));
+  QTT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_grid_kernel, 256, 0));
+  const int pairs = (k + 1) / 2;
+  int blocks = std::max(1, std::min((int)ceil_div(pairs, 8), per_sm * num_sms()));
+  double tol_v = tol;
+  void* args[] = {&p, &k, &X, &ldx, &W, &ldw, &tol_v, &flags};
+  QTT_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_grid_kernel, dim3(blocks), dim3(256), args, 0,
+                                       s));
+  QTT_CUDA(cudaFreeAsync(flags, s));
+  return kOk;
+}
+
+int sort_chop(cudaStream_t s, int p, int k, const double* X, int64_t ldx, double* sigma,
+              int* perm, const double* delta_dev, double delta_scale, int rmax, int floor_rule,
+              int* rank_dev) {
+  if (k <= 0 || k > SORT_MAX) return kUnsupported;
+  static bool configured = false;
+  if (!configured) {
+    QTT_CUDA(cudaFuncSetAttribute(sort_chop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(2 * SORT_MAX * sizeof(double))));
+    configured = true;
+  }
+  sort_chop_kernel<<<1, 1024, 2 * k * sizeof(double), s>>>(p, k, X, ldx, sigma, perm, delta_dev, delta_scale, rmax,
+                                      floor_rule, rank_dev);
+  QTT_CHECK_LAUNCH();
+  return kOk;
+}
+
+int frob_norm(cudaStream_t s, int64_t n, const double* x, double* out_dev) {
+  const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 1024), 1024));
+  double* part;
+  QTT_CUDA(cudaMallocAsync(&part, sizeof(double) * parts, s));
+  sumsq_partial_kernel<<<parts, 256, 0, s>>>(n, x, part);
+  QTT_CHECK_LAUNCH();
+  sum_final_kernel<<<1, 1024, 0, s>>>(parts, part, out_dev, 1);
+  QTT_CHECK_LAUNCH();
+  QTT_CUDA(cudaFreeAsync(part, s));
+  return kOk;
+}
+
+int no_truncation_certificate(cudaStream_t s, int k, const double* R, int64_t ldr,
+                              const double* delta_dev, double delta_scale, int* ok_dev) {
+  double *X, *T, *norms;
+  const int64_t kk = k;
+  QTT_CUDA(cudaMallocAsync(&X, sizeof(double) * kk * kk, s));
+  QTT_CUDA(cudaMallocAsync(&T, sizeof(double) * kk * kk, s));
+  QTT_CUDA(cudaMallocAsync(&norms, sizeof(double) * 2, s));
+  QTT_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * kk * kk, s));
+  static bool configured = false;
+  const int tri_smem = (int)(2 * TRB * (TRB + 1) * sizeof(double));
+  if (!configured) {
+    QTT_CUDA(cudaFuncSetAttribute(trinv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  tri_smem));
+    configured = true;
+  }
+  trinv_diag_kernel<<<(int)ceil_div(k, TRB), TRB, tri_smem, s>>>(k, R, ldr, X, kk);
+  QTT_CHECK_LAUNCH();
+  // Recursive doubling: X12 = -X11 * R12 * X22 for block pairs of size sz.
+  for (int sz = TRB; sz < k; sz *= 2) {
+    for (int b = 0; b + sz < k; b += 2 * sz) {
+      const int c = std::min(sz, k - b - sz);
+      const double* R12 = R + b + (int64_t)(b + sz) * ldr;
+      const double* X22 = X + (b + sz) + (int64_t)(b + sz) * kk;
+      const double* X11 = X + b + (int64_t)b * kk;
+      double* X12 = X + b + (int64_t)(b + sz) * kk;
+      QTT_TRY(dgemm(s, 0, 0, sz, c, c, 1.0, R12, ldr, X22, kk, 0.0, T, sz));
+      QTT_TRY(dgemm(s, 0, 0, sz, c, sz, -1.0, X11, kk, T, sz, 0.0, X12, kk));
+    }
+  }
+  // ||R||_F (upper triangle of R as stored: caller guarantees zeros below)
+  double* Rc;
+  QTT_CUDA(cudaMallocAsync(&Rc, sizeof(double) * kk * kk, s));
+  QTT_TRY(copy_matrix(s, k, k, R, ldr, Rc, kk));
+  QTT_TRY(frob_norm(s, kk * kk, Rc, norms));
+  QTT_TRY(frob_norm(s, kk * kk, X, norms + 1));
+  certificate_kernel<<<1, 1, 0, s>>>(k, norms, norms + 1, delta_dev, delta_scale, ok_dev);
+  QTT_CHECK_LAUNCH();
+  QTT_CUDA(cudaFreeAsync(Rc, s));
+  QTT_CUDA(cudaFreeAsync(X, s));
+  QTT_CUDA(cudaFreeAsync(T, s));
+  QTT_CUDA(cudaFreeAsync(norms, s));
+  return kOk;
+}
+
+int gather_columns(cudaStream_t s, int rows, int cols, const double* src, int64_t lds,
+                   const int* perm, double* dst, int64_t ldd) {
+  if (rows <= 0 || cols <= 0) return kOk;
+  gather_columns_kernel<<<grid_for((int64_t)rows * cols), 256, 0, s>>>(rows, cols, src, lds, perm,
+                                                                       dst, ldd);
+  QTT_CHECK_LAUNCH();
+  return kOk;
+}
+
+}  // namespace qtt

@@ -1,0 +1,46 @@
+// Dense FP64 building blocks for TT rounding / TT-SVD / AMEn (sm_100a).
+#pragma once
+#include "common.cuh"
+
+namespace qtt {
+
+// Householder QR of a column-major m x n matrix A (lda).  Writes the
+// explicit thin factor Q (m x k, ldq) and R (k x n upper triangular, ldr),
+// k = min(m, n).  A is not modified.  Blocked: panels of 32 columns are
+// factorised by one thread-block cluster (rows spread over up to 16 CTAs,
+// reductions through distributed shared memory), trailing updates and the
+// explicit-Q accumulation are compact-WY DMMA GEMMs.
+int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
+       double* R, int64_t ldr);
+
+// One-sided (Hestenes) Jacobi on the p x k column-major matrix X (ldx, in
+// place): X <- X W with W (k x k, ldw) orthogonal, so that the columns of X
+// become mutually orthogonal.  W is initialised to the identity here.
+int jacobi(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw);
+
+// Column norms of X (p x k) sorted descending: sigma[k] and perm[k] (device).
+// rank = chop(sigma, delta) (ttcore.py:175-190) with delta read from
+// *delta_dev (device scalar) times delta_scale, clamped to rmax; floor_rule
+// selects the reference rounding rule (eps floor) or the solver rule
+// without floor (solver.py:221-236).  *rank_dev receives the kept rank.
+int sort_chop(cudaStream_t s, int p, int k, const double* X, int64_t ldx, double* sigma,
+              int* perm, const double* delta_dev, double delta_scale, int rmax, int floor_rule,
+              int* rank_dev);
+
+// Certificate that truncation cannot happen: with R (k x k upper triangular)
+// sets *ok_dev = 1 iff 1/||R^{-1}||_F > 1.25 * max(delta, ||R||_F*max(k,2)*eps),
+// i.e. the smallest singular value of R provably exceeds the _chop threshold.
+int no_truncation_certificate(cudaStream_t s, int k, const double* R, int64_t ldr,
+                              const double* delta_dev, double delta_scale, int* ok_dev);
+
+// Gather columns: dst[:, c] = src[:, perm[c]] for c < cols (device perm).
+int gather_columns(cudaStream_t s, int rows, int cols, const double* src, int64_t lds,
+                   const int* perm, double* dst, int64_t ldd);
+
+// Frobenius norm of a contiguous array into a device scalar.
+int frob_norm(cudaStream_t s, int64_t n, const double* x, double* out_dev);
+
+// Identity into a column-major rows x cols matrix.
+int set_identity(cudaStream_t s, int rows, int cols, double* A, int64_t lda);
+
+}  // namespace qtt

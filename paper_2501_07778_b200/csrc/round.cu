@@ -1,0 +1,449 @@
+// TT rounding (row a5), orthogonal norm (a7) and TT-SVD (a6) on the device.
+//
+// Rounding follows ttcore.tt_round (ttcore.py:322-338): a right-to-left
+// Householder QR sweep (ttcore.py:296-306), then a left-to-right truncated
+// SVD sweep (ttcore.py:309-319) with delta = eps/sqrt(d-1)*||t||.  Each SVD
+// step first QR-factorises the unfolding; when the triangular factor
+// provably has no singular value at or below the _chop threshold (the
+// certificate in linalg.cu) the QR factors ARE a valid rank-preserving
+// split and the SVD is skipped; otherwise the triangular factor goes
+// through one-sided Jacobi, which is backward stable, so rank decisions
+// agree with LAPACK's except at near-ties.  The norm is taken from core 0
+// after orthogonalisation (exact up to rounding, no sqrt(eps) floor).
+#include <cmath>
+#include <vector>
+
+#include "../../include/qtt_b200.h"
+#include "linalg.cuh"
+
+namespace qtt {
+
+int64_t packed_size(const qtt_layout* L);  // abi.cu
+void pack_offsets(qtt_layout* L);          // abi.cu
+
+namespace {
+
+struct DevBuf {
+  double* p = nullptr;
+  cudaStream_t s = nullptr;
+  int alloc(cudaStream_t st, int64_t n) {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    s = st;
+    QTT_CUDA(cudaMallocAsync(&p, sizeof(double) * std::max<int64_t>(n, 1), st));
+    return kOk;
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+template <typename T>
+int fetch(cudaStream_t s, const T* dev, T* host) {
+  QTT_CUDA(cudaMemcpyAsync(host, dev, sizeof(T), cudaMemcpyDeviceToHost, s));
+  QTT_CUDA(cudaStreamSynchronize(s));
+  return kOk;
+}
+
+// Right-to-left orthogonalisation of merged order-3 cores held in slots.
+int qr_sweep_right(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vector<int64_t>& n,
+                   const std::vector<int64_t>& off, double* work, double* tq, double* tr,
+                   double* tc) {
+  for (int k = d - 1; k >= 1; --k) {
+    const int rows = (int)(n[k] * r[k + 1]);
+    const int cols = (int)r[k];
+    const int kk = std::min(rows, cols);
+    QTT_TRY(qr(s, rows, cols, work + off[k], rows, tq, rows, tr, kk));
+    QTT_CUDA(cudaMemcpyAsync(work + off[k], tq, sizeof(double) * rows * (int64_t)kk,
+                             cudaMemcpyDeviceToDevice, s));
+    const int prev = (int)(r[k - 1] * n[k - 1]);
+    QTT_TRY(dgemm(s, 0, 0, kk, prev, cols, 1.0, tr, kk, work + off[k - 1], cols, 0.0, tc, kk));
+    QTT_CUDA(cudaMemcpyAsync(work + off[k - 1], tc, sizeof(double) * kk * (int64_t)prev,
+                             cudaMemcpyDeviceToDevice, s));
+    r[k] = kk;
+  }
+  return kOk;
+}
+
+}  // namespace
+
+// Rounding core on merged order-3 slots (shared by qtt_round and the solver).
+int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vector<int64_t>& n,
+                const std::vector<int64_t>& off, double* work, double eps) {
+  if (d == 1) return kOk;
+  int64_t maxcore = 1;
+  for (int k = 0; k < d; ++k) maxcore = std::max(maxcore, r[k] * n[k] * r[k + 1]);
+  DevBuf tq, tr, tc, lc, xb, wb, wp, zp, sc;
+  QTT_TRY(tq.alloc(s, maxcore));
+  QTT_TRY(tr.alloc(s, maxcore));
+  QTT_TRY(tc.alloc(s, maxcore));
+  QTT_TRY(lc.alloc(s, maxcore));
+  QTT_TRY(xb.alloc(s, maxcore));
+  QTT_TRY(wb.alloc(s, maxcore));
+  QTT_TRY(wp.alloc(s, maxcore));
+  QTT_TRY(zp.alloc(s, maxcore));
+  QTT_TRY(sc.alloc(s, 64 + 3 * maxcore));
+  double* norm_dev = sc.p;
+  double* sigma = sc.p + 8;
+  int* perm = reinterpret_cast<int*>(sc.p + 8 + maxcore);
+  int* flags = reinterpret_cast<int*>(sc.p + 2);  // [0]: cert ok, [1]: rank
+
+  QTT_TRY(qr_sweep_right(s, d, r, n, off, work, tq.p, tr.p, tc.p));
+  QTT_TRY(frob_norm(s, r[0] * n[0] * r[1], work + off[0], norm_dev));
+  const double dscale = eps / std::sqrt((double)std::max(d - 1, 1));
+
+  for (int k = 0; k < d - 1; ++k) {
+    const int m = (int)(r[k] * n[k]);
+    const int N = (int)r[k + 1];
+    const int mc = (int)(n[k + 1] * r[k + 2]);  // rows of the next core's column-major view
+    double* core = work + off[k];
+    double* next = work + off[k + 1];
+    int newk;
+    if (m >= N) {
+      // tall: L (m x N) row-major == core; factor its column-major copy
+      QTT_TRY(transpose(s, N, m, core, N, lc.p, m));
+      QTT_TRY(qr(s, m, N, lc.p, m, tq.p, m, tr.p, N));
+      QTT_TRY(no_truncation_certificate(s, N, tr.p, N, norm_dev, dscale, flags));
+      int ok = 0;
+      QTT_TRY(fetch(s, flags, &ok));
+      if (ok) {
+        newk = N;
+        QTT_TRY(transpose(s, m, N, tq.p, m, core, N));
+        QTT_TRY(dgemm(s, 0, 1, mc, N, N, 1.0, next, mc, tr.p, N, 0.0, tc.p, mc));
+      } else {
+        QTT_TRY(transpose(s, N, N, tr.p, N, xb.p, N));  // X = R^T
+        QTT_TRY(jacobi(s, N, N, xb.p, N, wb.p, N));
+        QTT_TRY(sort_chop(s, N, N, xb.p, N, sigma, perm, norm_dev, dscale, N, 1, flags + 1));
+        QTT_TRY(fetch(s, flags + 1, &newk));
+        QTT_TRY(gather_columns(s, N, newk, wb.p, N, perm, wp.p, N));
+        QTT_TRY(dgemm(s, 0, 0, m, newk, N, 1.0, tq.p, m, wp.p, N, 0.0, lc.p, m));
+        QTT_TRY(transpose(s, m, newk, lc.p, m, core, newk));
+        QTT_TRY(gather_columns(s, N, newk, xb.p, N, perm, zp.p, N));
+        QTT_TRY(dgemm(s, 0, 0, mc, newk, N, 1.0, next, mc, zp.p, N, 0.0, tc.p, mc));
+      }
+    } else {
+      // wide: L^T (N x m) column-major == core memory
+      QTT_TRY(qr(s, N, m, core, N, nullptr, 1, tr.p, m));
+      QTT_TRY(no_truncation_certificate(s, m, tr.p, m, norm_dev, dscale, flags));
+      int ok = 0;
+      QTT_TRY(fetch(s, flags, &ok));
+      if (ok) {
+        newk = m;
+        QTT_TRY(dgemm(s, 0, 0, mc, m, N, 1.0, next, mc, core, N, 0.0, tc.p, mc));
+        QTT_TRY(set_identity(s, m, m, core, m));
+      } else {
+        QTT_TRY(copy_matrix(s, m, m, tr.p, m, xb.p, m));  // X = R2 (S = R2^T)
+        QTT_TRY(jacobi(s, m, m, xb.p, m, wb.p, m));
+        QTT_TRY(sort_chop(s, m, m, xb.p, m, sigma, perm, norm_dev, dscale, m, 1, flags + 1));
+        QTT_TRY(fetch(s, flags + 1, &newk));
+        QTT_TRY(gather_columns(s, m, newk, wb.p, m, perm, wp.p, m));
+        QTT_TRY(dgemm(s, 0, 0, N, newk, m, 1.0, core, N, wp.p, m, 0.0, lc.p, N));  // carry^T
+        QTT_TRY(dgemm(s, 0, 0, mc, newk, N, 1.0, next, mc, lc.p, N, 0.0, tc.p, mc));
+        QTT_TRY(transpose(s, m, newk, wp.p, m, core, newk));
+      }
+    }
+    QTT_CUDA(cudaMemcpyAsync(next, tc.p, sizeof(double) * (int64_t)mc * newk,
+                             cudaMemcpyDeviceToDevice, s));
+    r[k + 1] = newk;
+  }
+  return kOk;
+}
+
+int round_tt(const qtt_layout* in, const double* in_data, double eps, qtt_layout* out,
+             double* out_data, cudaStream_t s) {
+  const int d = in->d;
+  if (d < 1 || d > QTT_MAX_CORES || eps < 0) return kInvalid;
+  std::vector<int64_t> r(d + 1), n(d), off(d);
+  for (int k = 0; k <= d; ++k) r[k] = in->ranks[k];
+  for (int k = 0; k < d; ++k) {
+    n[k] = in->rows[k] * in->cols[k];
+    off[k] = in->offsets[k];
+  }
+  const int64_t total = packed_size(in);
+  DevBuf work;
+  QTT_TRY(work.alloc(s, total));
+  QTT_CUDA(cudaMemcpyAsync(work.p, in_data, sizeof(double) * total, cudaMemcpyDeviceToDevice, s));
+  QTT_TRY(round_slots(s, d, r, n, off, work.p, eps));
+  *out = *in;
+  for (int k = 0; k <= d; ++k) out->ranks[k] = r[k];
+  pack_offsets(out);
+  for (int k = 0; k < d; ++k)
+    QTT_CUDA(cudaMemcpyAsync(out_data + out->offsets[k], work.p + off[k],
+                             sizeof(double) * r[k] * n[k] * r[k + 1], cudaMemcpyDeviceToDevice,
+                             s));
+  QTT_CUDA(cudaStreamSynchronize(s));
+  return kOk;
+}
+
+// ||t|| after right-to-left orthogonalisation (accurate for cancelling sums).
+int norm_orth(const qtt_layout* in, const double* in_data, double* result, cudaStream_t s) {
+  const int d = in->d;
+  if (d < 1 || d > QTT_MAX_CORES) return kInvalid;
+  std::vector<int64_t> r(d + 1), n(d), off(d);
+  for (int k = 0; k <= d; ++k) r[k] = in->ranks[k];
+  for (int k = 0; k < d; ++k) {
+    n[k] = in->rows[k] * in->cols[k];
+    off[k] = in->offsets[k];
+  }
+  int64_t maxcore = 1;
+  for (int k = 0; k < d; ++k) maxcore = std::max(maxcore, r[k] * n[k] * r[k + 1]);
+  const int64_t total = packed_size(in);
+  DevBuf work, tq, tr, tc, nb;
+  QTT_TRY(work.alloc(s, total));
+  QTT_TRY(tq.alloc(s, maxcore));
+  QTT_TRY(tr.alloc(s, maxcore));
+  QTT_TRY(tc.alloc(s, maxcore));
+  QTT_TRY(nb.alloc(s, 1));
+  QTT_CUDA(cudaMemcpyAsync(work.p, in_data, sizeof(double) * total, cudaMemcpyDeviceToDevice, s));
+  QTT_TRY(qr_sweep_right(s, d, r, n, off, work.p, tq.p, tr.p, tc.p));
+  QTT_TRY(frob_norm(s, r[0] * n[0] * r[1], work.p + off[0], nb.p));
+  return fetch(s, nb.p, result);
+}
+
+// ------------------------------------------------------------------ TT-SVD
+namespace {
+
+constexpr int TSQR_THREADS = 256;
+
+// R factor (upper m x m, row-major into the stack) of a BR x m block of the
+// row-major tall matrix src (rows x m).  Unblocked Householder in smem.
+__global__ void __launch_bounds__(TSQR_THREADS) tsqr_leaf_kernel(int64_t rows, int m, int br,
+                                                                 const double* __restrict__ src,
+                                                                 double* __restrict__ dst) {
+  extern __shared__ double ts[];
+  __shared__ double red[TSQR_THREADS / 32];
+  __shared__ double wv[64];
+  const int64_t r0 = (int64_t)blockIdx.x * br;
+  const int nr = (int)std::min<int64_t>(br, rows - r0);
+  double* P = ts;  // col-major nr x m, ld br
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < nr * m; idx += TSQR_THREADS) {
+    const int rr = idx / m, c = idx % m;
+    P[rr + c * br] = src[(r0 + rr) * m + c];
+  }
+  __syncthreads();
+  const int kmax = min(nr, m);
+  for (int j = 0; j < kmax; ++j) {
+    double sq = 0.0;
+    for (int rr = j + 1 + tid; rr < nr; rr += TSQR_THREADS) {
+      const double x = P[rr + j * br];
+      sq = fma(x, x, sq);
+    }
+    sq = warp_sum(sq);
+    if (lane == 0) red[warp] = sq;
+    __syncthreads();
+    double norm2 = 0.0;
+    for (int w = 0; w < TSQR_THREADS / 32; ++w) norm2 += red[w];
+    const double alpha = P[j + j * br];
+    double tau = 0.0, beta = alpha, scal = 1.0;
+    if (norm2 > 0.0) {
+      const double nrm = sqrt(fma(alpha, alpha, norm2));
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    __syncthreads();
+    for (int rr = j + 1 + tid; rr < nr; rr += TSQR_THREADS) P[rr + j * br] *= scal;
+    if (tid == 0) P[j + j * br] = beta;
+    __syncthreads();
+    if (tau != 0.0) {
+      for (int c = j + 1 + warp; c < m; c += TSQR_THREADS / 32) {
+        double part = 0.0;
+        for (int rr = j + 1 + lane; rr < nr; rr += 32) part = fma(P[rr + j * br], P[rr + c * br], part);
+        part = warp_sum(part);
+        if (lane == 0) wv[c] = tau * (P[j + c * br] + part);
+      }
+      __syncthreads();
+      for (int idx = tid; idx < (nr - j) * (m - j - 1); idx += TSQR_THREADS) {
+        const int rr = j + idx % (nr - j);
+        const int c = j + 1 + idx / (nr - j);
+        const double v = (rr == j) ? 1.0 : P[rr + j * br];
+        P[rr + c * br] = fma(-wv[c], v, P[rr + c * br]);
+      }
+      __syncthreads();
+    }
+  }
+  // write R (m x m upper, rows beyond kmax zero) row-major
+  double* out = dst + (int64_t)blockIdx.x * m * m;
+  for (int idx = tid; idx < m * m; idx += TSQR_THREADS) {
+    const int i = idx / m, c = idx % m;
+    out[idx] = (i <= c && i < kmax) ? P[i + c * br] : 0.0;
+  }
+}
+
+__global__ void write_core_kernel(int rp, int n, int rk, const double* __restrict__ U, int ldu,
+                                  const int* __restrict__ perm, double* __restrict__ core) {
+  // core[a, i, c] = U[a + rp*i, perm[c]]
+  const int total = rp * n * rk;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int c = idx % rk;
+    const int t = idx / rk;
+    const int i = t % n, a = t / n;
+    core[idx] = U[(a + rp * i) + (int64_t)perm[c] * ldu];
+  }
+}
+
+__global__ void iota_kernel(int n, int* p) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
+}
+
+__global__ void zero_check_kernel(const double* nrm, int* is_zero) { *is_zero = (*nrm == 0.0); }
+
+// R factor of a row-major (rows x m) tall matrix, m <= 64, into R (m x m, col-major ld m).
+int tsqr_r(cudaStream_t s, int64_t rows, int m, const double* src, double* R) {
+  int br = (int)std::min<int64_t>(4096, std::max<int64_t>(2 * m, 8192 / m));
+  br = (br + 31) / 32 * 32;
+  const size_t smem = sizeof(double) * (size_t)br * m;
+  static bool configured = false;
+  if (!configured) {
+    QTT_CUDA(cudaFuncSetAttribute(tsqr_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  100 * 1024));
+    configured = true;
+  }
+  const double* cur = src;
+  int64_t cur_rows = rows;
+  double* bufs[2] = {nullptr, nullptr};
+  DevBuf b0, b1;
+  const int64_t blocks0 = ceil_div(rows, br);
+  QTT_TRY(b0.alloc(s, blocks0 * m * m));
+  QTT_TRY(b1.alloc(s, ceil_div(blocks0 * m, br) * m * m + m * m));
+  bufs[0] = b0.p;
+  bufs[1] = b1.p;
+  int which = 0;
+  while (true) {
+    const int64_t blocks = ceil_div(cur_rows, br);
+    if (blocks > 0x7fffffff) return kUnsupported;
+    tsqr_leaf_kernel<<<(unsigned)blocks, TSQR_THREADS, smem, s>>>(cur_rows, m, br, cur, bufs[which]);
+    QTT_CHECK_LAUNCH();
+    cur = bufs[which];
+    cur_rows = blocks * m;
+    which ^= 1;
+    if (blocks == 1) break;
+  }
+  // cur holds R row-major (m x m): transpose into column-major R
+  return transpose(s, m, m, cur, m, R, m);
+}
+
+}  // namespace
+
+int decompose(const double* dense, int d, const int64_t* sizes, double eps, qtt_layout* out,
+              double* out_data, int64_t capacity, cudaStream_t s) {
+  if (d < 1 || d > QTT_MAX_CORES || eps < 0) return kInvalid;
+  int64_t total = 1;
+  for (int l = 0; l < d; ++l) {
+    if (sizes[l] < 1) return kInvalid;
+    total *= sizes[l];
+  }
+  out->d = d;
+  out->is_matrix = 0;
+  for (int l = 0; l < d; ++l) {
+    out->rows[l] = sizes[l];
+    out->cols[l] = 1;
+  }
+  DevBuf sc;
+  QTT_TRY(sc.alloc(s, 16));
+  double* nrm = sc.p;
+  int* izero = reinterpret_cast<int*>(sc.p + 1);
+  int* rank_dev = reinterpret_cast<int*>(sc.p + 2);
+  QTT_TRY(frob_norm(s, total, dense, nrm));
+  zero_check_kernel<<<1, 1, 0, s>>>(nrm, izero);
+  QTT_CHECK_LAUNCH();
+  int is_zero = 0;
+  QTT_TRY(fetch(s, izero, &is_zero));
+  if (is_zero) {
+    for (int l = 0; l <= d; ++l) out->ranks[l] = 1;
+    pack_offsets(out);
+    if (packed_size(out) > capacity) return kWorkspace;
+    QTT_CUDA(cudaMemsetAsync(out_data, 0, sizeof(double) * packed_size(out), s));
+    QTT_CUDA(cudaStreamSynchronize(s));
+    return kOk;
+  }
+  const double dscale = eps / std::sqrt((double)std::max(d - 1, 1));
+  // Cores are produced one by one into a staging list, packed at the end.
+  std::vector<DevBuf> cores(d);
+  std::vector<int64_t> rk(d + 1, 1);
+  DevBuf carry[2];
+  const double* cur = dense;
+  int64_t rest = total;
+  int rp = 1;
+  DevBuf R, W, Xb, sig, permb, Ub, Qb, Zp;
+  for (int l = 0; l < d - 1; ++l) {
+    const int n = (int)sizes[l];
+    const int m = rp * n;
+    const int64_t N = rest / n;
+    int newk;
+    DevBuf& nxt = carry[l & 1];
+    if (N >= m && m <= 64) {
+      QTT_TRY(R.alloc(s, (int64_t)m * m));
+      QTT_TRY(tsqr_r(s, N, m, cur, R.p));
+      QTT_TRY(W.alloc(s, (int64_t)m * m));
+      QTT_TRY(sig.alloc(s, 2 * m + 8));
+      int* perm = reinterpret_cast<int*>(sig.p + m + 4);
+      QTT_TRY(jacobi(s, m, m, R.p, m, W.p, m));  // R W = Z, U = W
+      QTT_TRY(sort_chop(s, m, m, R.p, m, sig.p, perm, nrm, dscale, m, 1, rank_dev));
+      QTT_TRY(fetch(s, rank_dev, &newk));
+      QTT_TRY(cores[l].alloc(s, (int64_t)rp * n * newk));
+      write_core_kernel<<<64, 256, 0, s>>>(rp, n, newk, W.p, m, perm, cores[l].p);
+      QTT_CHECK_LAUNCH();
+      // carry (newk x N) = U_k^T C  with C column-major (m x N)
+      QTT_TRY(Ub.alloc(s, (int64_t)m * newk));
+      QTT_TRY(gather_columns(s, m, newk, W.p, m, perm, Ub.p, m));
+      QTT_TRY(nxt.alloc(s, (int64_t)newk * N));
+      QTT_TRY(dgemm(s, 1, 0, newk, (int)N, m, 1.0, Ub.p, m, cur, m, 0.0, nxt.p, newk));
+    } else {
+      // tall (or too wide for TSQR): C (m x N) column-major; QR then Jacobi on R^T
+      const int kk = (int)std::min<int64_t>(m, N);
+      QTT_TRY(Qb.alloc(s, (int64_t)m * kk));
+      QTT_TRY(R.alloc(s, (int64_t)kk * N));
+      QTT_TRY(qr(s, m, (int)N, cur, m, Qb.p, m, R.p, kk));
+      // X = R^T (N x kk)
+      QTT_TRY(Xb.alloc(s, N * kk));
+      QTT_TRY(transpose(s, kk, (int)N, R.p, kk, Xb.p, N));
+      QTT_TRY(W.alloc(s, (int64_t)kk * kk));
+      QTT_TRY(jacobi(s, (int)N, kk, Xb.p, N, W.p, kk));  // R^T W = Z: R = W Z^T
+      QTT_TRY(sig.alloc(s, 2 * kk + 8));
+      int* perm = reinterpret_cast<int*>(sig.p + kk + 4);
+      QTT_TRY(sort_chop(s, (int)N, kk, Xb.p, N, sig.p, perm, nrm, dscale, kk, 1, rank_dev));
+      QTT_TRY(fetch(s, rank_dev, &newk));
+      // U = Q W_perm (m x newk); carry = Z_perm^T (newk x N)
+      QTT_TRY(Zp.alloc(s, (int64_t)kk * newk));
+      QTT_TRY(gather_columns(s, kk, newk, W.p, kk, perm, Zp.p, kk));
+      QTT_TRY(Ub.alloc(s, (int64_t)m * newk));
+      QTT_TRY(dgemm(s, 0, 0, m, newk, kk, 1.0, Qb.p, m, Zp.p, kk, 0.0, Ub.p, m));
+      DevBuf ip;
+      QTT_TRY(ip.alloc(s, newk));
+      iota_kernel<<<1, 256, 0, s>>>(newk, reinterpret_cast<int*>(ip.p));
+      QTT_CHECK_LAUNCH();
+      QTT_TRY(cores[l].alloc(s, (int64_t)rp * n * newk));
+      write_core_kernel<<<64, 256, 0, s>>>(rp, n, newk, Ub.p, m, reinterpret_cast<int*>(ip.p),
+                                           cores[l].p);
+      QTT_CHECK_LAUNCH();
+      QTT_TRY(nxt.alloc(s, (int64_t)newk * N));
+      DevBuf zc;
+      QTT_TRY(zc.alloc(s, N * newk));
+      QTT_TRY(gather_columns(s, (int)N, newk, Xb.p, N, perm, zc.p, N));
+      QTT_TRY(transpose(s, (int)N, newk, zc.p, N, nxt.p, newk));
+    }
+    rk[l + 1] = newk;
+    cur = nxt.p;
+    rest = N;
+    rp = newk;
+  }
+  // last core: (rp, n, 1) from cur (rp x n column-major) -> row-major
+  const int nlast = (int)sizes[d - 1];
+  QTT_TRY(cores[d - 1].alloc(s, (int64_t)rp * nlast));
+  QTT_TRY(transpose(s, rp, nlast, cur, rp, cores[d - 1].p, nlast));
+  for (int l = 0; l <= d; ++l) out->ranks[l] = rk[l];
+  out->ranks[0] = 1;
+  out->ranks[d] = 1;
+  pack_offsets(out);
+  if (packed_size(out) > capacity) return kWorkspace;
+  for (int l = 0; l < d; ++l)
+    QTT_CUDA(cudaMemcpyAsync(out_data + out->offsets[l], cores[l].p,
+                             sizeof(double) * rk[l] * sizes[l] * rk[l + 1],
+                             cudaMemcpyDeviceToDevice, s));
+  QTT_CUDA(cudaStreamSynchronize(s));
+  return kOk;
+}
+
+}  // namespace qtt

@@ -1,0 +1,207 @@
+"""Parity of the device TT algebra (C ABI) against the numpy oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tt as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _T():
+    from paper_2501_07778_b200 import ttcore as T
+
+    return T
+
+
+def rand_vec(rng, d, r, n=2):
+    rk = [1] + [r] * (d - 1) + [1]
+    return [rng.standard_normal((rk[k], n, rk[k + 1])) for k in range(d)]
+
+
+def rand_mat(rng, d, r, n=2, m=2):
+    rk = [1] + [r] * (d - 1) + [1]
+    return [rng.standard_normal((rk[k], n, m, rk[k + 1])) for k in range(d)]
+
+
+def dense_of(t):
+    return _T().tt_contract(t)
+
+
+def test_gemm_all_transposes():
+    T = _T()
+    rng = np.random.default_rng(0)
+    for ta in (0, 1):
+        for tb in (0, 1):
+            m, n, k = 70, 45, 33
+            a = rng.standard_normal((k, m) if ta else (m, k))
+            b = rng.standard_normal((n, k) if tb else (k, n))
+            c0 = rng.standard_normal((m, n))
+            # column-major buffers: store transposes of C-order arrays
+            A = torch.tensor(np.asfortranarray(a).ravel(order="F"), device="cuda")
+            B = torch.tensor(np.asfortranarray(b).ravel(order="F"), device="cuda")
+            C = torch.tensor(c0.ravel(order="F"), device="cuda")
+            T._gemm(ta, tb, m, n, k, 0.5, A, a.shape[0], B, b.shape[0], 2.0, C, m)
+            want = 0.5 * (a.T if ta else a) @ (b.T if tb else b) + 2.0 * c0
+            got = C.cpu().numpy().reshape((n, m)).T
+            assert np.abs(got - want).max() < 1e-12 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("m,n", [(5, 3), (64, 64), (300, 40), (100, 150), (2000, 96), (4100, 70)])
+def test_qr_explicit(m, n):
+    from paper_2501_07778_b200 import _lib
+    import ctypes
+
+    rng = np.random.default_rng(m + n)
+    a = rng.standard_normal((m, n))
+    k = min(m, n)
+    A = torch.tensor(a.ravel(order="F"), device="cuda")
+    Q = torch.zeros(m * k, dtype=torch.float64, device="cuda")
+    R = torch.zeros(k * n, dtype=torch.float64, device="cuda")
+    _lib.call("qtt_qr", ctypes.c_int64(m), ctypes.c_int64(n), _lib.ptr(A), ctypes.c_int64(m),
+              _lib.ptr(Q), ctypes.c_int64(m), _lib.ptr(R), ctypes.c_int64(k), _lib.stream_handle())
+    q = Q.cpu().numpy().reshape(k, m).T
+    r = R.cpu().numpy().reshape(n, k).T
+    assert np.abs(q @ r - a).max() < 1e-12 * np.abs(a).max() * max(m, n) ** 0.5
+    assert np.abs(q.T @ q - np.eye(k)).max() < 1e-13 * max(m, n)
+    assert np.allclose(np.tril(r, -1), 0.0)
+
+
+@pytest.mark.parametrize("m,n", [(6, 4), (50, 50), (120, 80), (40, 90), (400, 300)])
+def test_svd_values_and_vectors(m, n):
+    from paper_2501_07778_b200 import _lib
+    import ctypes
+
+    rng = np.random.default_rng(7 * m + n)
+    k = min(m, n)
+    # graded spectrum down to 1e-14 relative
+    u0, _ = np.linalg.qr(rng.standard_normal((m, k)))
+    v0, _ = np.linalg.qr(rng.standard_normal((n, k)))
+    s0 = np.logspace(0, -14, k)
+    a = (u0 * s0) @ v0.T
+    A = torch.tensor(a.ravel(order="F"), device="cuda")
+    S = torch.zeros(k, dtype=torch.float64, device="cuda")
+    U = torch.zeros(m * k, dtype=torch.float64, device="cuda")
+    _lib.call("qtt_svd", ctypes.c_int64(m), ctypes.c_int64(n), _lib.ptr(A), ctypes.c_int64(m),
+              _lib.ptr(S), _lib.ptr(U), ctypes.c_int64(m), _lib.stream_handle())
+    s = S.cpu().numpy()
+    s_ref = np.linalg.svd(a, compute_uv=False)
+    assert np.abs(s - s_ref).max() <= 1e-14 * s_ref[0] * 10
+    u = U.cpu().numpy().reshape(k, m).T
+    assert np.abs(u.T @ u - np.eye(k)).max() < 1e-12
+    # leading singular subspace matches
+    top = 5
+    proj = u[:, :top].T @ np.linalg.svd(a)[0][:, :top]
+    assert np.allclose(np.abs(np.linalg.svd(proj, compute_uv=False)), 1.0, atol=1e-10)
+
+
+def test_matvec_matmat_hadamard_add():
+    T = _T()
+    rng = np.random.default_rng(1)
+    A = rand_mat(rng, 6, 3)
+    B = rand_mat(rng, 6, 2)
+    x = rand_vec(rng, 6, 4)
+    y = rand_vec(rng, 6, 2)
+    TA, TB, tx, ty = T.TTMatrix(A), T.TTMatrix(B), T.TTVector(x), T.TTVector(y)
+    assert np.abs(dense_of(T.tt_matvec(TA, tx)) - O.full(O.matvec(A, x))).max() < 1e-12
+    assert np.abs(dense_of(T.tt_matmat(TA, TB)) - O.full(O.matmat(A, B))).max() < 1e-11
+    assert np.abs(dense_of(T.tt_hadamard(tx, ty)) - O.full(O.hadamard(x, y))).max() < 1e-12
+    assert np.abs(dense_of(T.tt_hadamard(TA, TB)) - O.full(O.hadamard(A, B))).max() < 1e-12
+    assert np.abs(dense_of(T.tt_add(tx, ty)) - O.full(O.add(x, y))).max() < 1e-12
+    assert np.abs(dense_of(T.tt_add(TA, TB)) - O.full(O.add(A, B))).max() < 1e-12
+    assert np.abs(dense_of(T.tt_scale(TA, -2.5)) - O.full(O.scale(A, -2.5))).max() < 1e-12
+    assert np.abs(dense_of(T.tt_transpose(TA)) - O.full(A).T).max() < 1e-12
+    assert np.abs(dense_of(T.tt_diag(tx)) - np.diag(O.full(x))).max() < 1e-12
+    # ranks follow the reference rules
+    assert T.tt_matvec(TA, tx).ranks == O.ranks(O.matvec(A, x))
+    assert T.tt_add(tx, ty).ranks == O.ranks(O.add(x, y))
+
+
+def test_zkron_kron_slice():
+    T = _T()
+    rng = np.random.default_rng(2)
+    a, b = rand_vec(rng, 3, 2), rand_vec(rng, 3, 3)
+    A, B = rand_mat(rng, 3, 2), rand_mat(rng, 3, 2)
+    assert np.abs(dense_of(T.tt_zkron(T.TTVector(a), T.TTVector(b))) - O.full(O.zkron(a, b))).max() < 1e-12
+    assert np.abs(dense_of(T.tt_zkron(T.TTMatrix(A), T.TTMatrix(B))) - O.full(O.zkron(A, B))).max() < 1e-12
+    assert np.abs(dense_of(T.tt_kron(T.TTMatrix(A), T.TTMatrix(B))) - O.full(O.kron(A, B))).max() < 1e-12
+    v = rand_vec(rng, 5, 3)
+    for mode in (0, 2, 4):
+        got = dense_of(T.tt_slice_mode(T.TTVector(v), mode, 1))
+        assert np.abs(got - O.full(O.slice_mode(v, mode, 1))).max() < 1e-12
+
+
+def test_norm_dot_contract_apply():
+    T = _T()
+    rng = np.random.default_rng(3)
+    x = rand_vec(rng, 8, 5)
+    y = rand_vec(rng, 8, 3)
+    tx, ty = T.TTVector(x), T.TTVector(y)
+    assert abs(T.tt_norm(tx) - np.linalg.norm(O.full(x))) < 1e-12 * np.linalg.norm(O.full(x))
+    assert abs(T.tt_dot(tx, ty) - O.full(x) @ O.full(y)) < 1e-11 * np.linalg.norm(O.full(x)) * np.linalg.norm(O.full(y))
+    A = rand_mat(rng, 6, 4)
+    v = rng.standard_normal(64)
+    from paper_2501_07778_b200 import solver
+
+    got = solver.apply_tt_matrix(T.TTMatrix(A), v)
+    got = got.cpu().numpy() if hasattr(got, "cpu") else got
+    assert np.abs(got - O.full(A) @ v).max() < 1e-11
+
+
+@pytest.mark.parametrize("eps", [1e-2, 1e-6, 1e-10])
+def test_round_ranks_and_error(eps):
+    T = _T()
+    rng = np.random.default_rng(4)
+    for trial in range(6):
+        x = rand_vec(rng, 7, 3 + trial % 3)
+        z = O.add(O.add(x, O.scale(x, 0.5)), rand_vec(rng, 7, 2))
+        ref = O.round_tt(z, eps)
+        got = T.tt_round(T.TTVector(z), eps)
+        assert got.ranks == O.ranks(ref)
+        full = O.full(z)
+        err = np.linalg.norm(dense_of(got) - full) / np.linalg.norm(full)
+        assert err <= eps * (1 + 1e-8) + 1e-13
+
+
+def test_round_matrix():
+    T = _T()
+    rng = np.random.default_rng(5)
+    A = rand_mat(rng, 5, 3)
+    z = O.add(A, O.scale(A, 2.0))
+    ref = O.round_tt(z, 1e-12)
+    got = T.tt_round(T.TTMatrix(z), 1e-12)
+    assert got.ranks == O.ranks(ref)
+    assert np.abs(dense_of(got) - O.full(z)).max() < 1e-10
+
+
+@pytest.mark.parametrize("eps", [0.0, 1e-3, 1e-8])
+def test_decompose_vector(eps):
+    T = _T()
+    rng = np.random.default_rng(6)
+    xs = np.linspace(0, 1, 1 << 12)
+    v = np.sin(3 * xs) * np.exp(-xs) + 0.01 * rng.standard_normal(xs.size) * (eps == 0.0)
+    ref = O.decompose_vector(v, eps)
+    got = T.tt_decompose(v, eps)
+    if eps > 0:
+        assert got.ranks == O.ranks(ref)
+    err = np.linalg.norm(dense_of(got) - v) / np.linalg.norm(v)
+    assert err <= max(eps, 1e-13)
+
+
+def test_decompose_matrix_and_zero():
+    T = _T()
+    rng = np.random.default_rng(8)
+    m = rng.standard_normal((16, 16))
+    got = T.tt_decompose(m, 0.0)
+    assert np.abs(dense_of(got) - m).max() < 1e-12
+    z = T.tt_decompose(np.zeros(8), 0.0)
+    assert z.ranks == (1, 1, 1, 1)
+
+
+def test_zorder_maps_bit_exact():
+    from paper_2501_07778_b200 import indexing
+
+    for d in (1, 3, 6):
+        assert np.array_equal(indexing.zorder_permutation(d), O.zorder_permutation(d))
+        assert np.array_equal(indexing.zorder_dof_permutation(d), O.zorder_dof_permutation(d))
