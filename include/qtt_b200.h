@@ -55,6 +55,15 @@ typedef struct qtt_layout {
 /* Library identification; returns a static string. */
 const char* qtt_version(void);
 
+/* Kernel launches issued by the library since load (bench.py evidence). */
+long long qtt_launch_count(void);
+
+/* DMMA GEMM profiling: qtt_profile_gemm(1) starts recording CUDA events
+ * around every GEMM launch (on its stream); _read returns the summed
+ * algorithmic FLOPs (2mnk), the summed event time and the launch count. */
+int qtt_profile_gemm(int32_t on);
+int qtt_profile_gemm_read(double* flops, double* ms, int64_t* launches);
+
 /* Number of doubles a packed buffer for `lay` needs (with alignment). */
 int64_t qtt_layout_size(const qtt_layout* lay);
 

@@ -20,6 +20,9 @@ QTT_OK, QTT_EINVAL, QTT_ECUDA, QTT_EWORKSPACE, QTT_EUNSUPPORTED = range(5)
 # Every symbol declared in include/qtt_b200.h (checked by tests/test_abi.py).
 EXPORTS = (
     "qtt_version",
+    "qtt_launch_count",
+    "qtt_profile_gemm",
+    "qtt_profile_gemm_read",
     "qtt_layout_size",
     "qtt_matvec",
     "qtt_matmat",
@@ -80,8 +83,9 @@ def load():
         lib = ctypes.CDLL(_LIB_PATH)
         lib.qtt_version.restype = ctypes.c_char_p
         lib.qtt_layout_size.restype = ctypes.c_int64
+        lib.qtt_launch_count.restype = ctypes.c_longlong
         for name in EXPORTS:
-            if name not in ("qtt_version", "qtt_layout_size"):
+            if name not in ("qtt_version", "qtt_layout_size", "qtt_launch_count"):
                 getattr(lib, name).restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -123,3 +127,19 @@ def call(name: str, *args) -> None:
 
 def align(n: int) -> int:
     return (n + 31) // 32 * 32
+
+
+def launch_count() -> int:
+    return int(load().qtt_launch_count())
+
+
+def gemm_profile_start() -> None:
+    call("qtt_profile_gemm", ctypes.c_int32(1))
+
+
+def gemm_profile_stop() -> tuple:
+    """(flops, ms, launches) of the GEMMs since gemm_profile_start()."""
+    f, ms, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+    call("qtt_profile_gemm_read", ctypes.byref(f), ctypes.byref(ms), ctypes.byref(n))
+    call("qtt_profile_gemm", ctypes.c_int32(0))
+    return f.value, ms.value, n.value

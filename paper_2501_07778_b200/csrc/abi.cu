@@ -1,4 +1,5 @@
 // extern "C" boundary of libqttb200.so (declared in include/qtt_b200.h).
+#include <atomic>
 #include <cstring>
 
 #include "../../include/qtt_b200.h"
@@ -46,6 +47,9 @@ int dense_apply(const qtt_layout*, const double*, const double*, double*, cudaSt
 int zorder_perm(int, int64_t*, int, cudaStream_t);
 int z_index(int, int64_t, const int64_t*, const int64_t*, int64_t*, cudaStream_t);
 
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 namespace {
 inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 bool valid(const qtt_layout* L) {
@@ -66,6 +70,36 @@ using namespace qtt;
 extern "C" {
 
 const char* qtt_version(void) { return "qtt_b200 0.1 sm_100a fp64"; }
+
+long long qtt_launch_count(void) { return g_launches.load(); }
+
+int qtt_profile_gemm(int32_t on) {
+  GemmProfile& p = gemm_profile();
+  for (auto& e : p.events) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  p.events.clear();
+  p.launch_flops.clear();
+  p.flops = 0.0;
+  p.on = on != 0;
+  return QTT_OK;
+}
+
+int qtt_profile_gemm_read(double* flops, double* ms, int64_t* launches) {
+  GemmProfile& p = gemm_profile();
+  double tot = 0.0;
+  for (auto& e : p.events) {
+    QTT_CUDA(cudaEventSynchronize(e.second));
+    float t = 0.f;
+    QTT_CUDA(cudaEventElapsedTime(&t, e.first, e.second));
+    tot += t;
+  }
+  *flops = p.flops;
+  *ms = tot;
+  *launches = (int64_t)p.events.size();
+  return QTT_OK;
+}
 
 int64_t qtt_layout_size(const qtt_layout* lay) { return valid(lay) ? packed_size(lay) : -1; }
 

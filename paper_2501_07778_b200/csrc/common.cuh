@@ -5,6 +5,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <algorithm>
+#include <utility>
+#include <vector>
 
 namespace qtt {
 
@@ -30,7 +32,14 @@ constexpr int kMaxCores = 96;  // QTT depth supported by by-value descriptors
     }                                                                      \
   } while (0)
 
-#define QTT_CHECK_LAUNCH() QTT_CUDA(cudaGetLastError())
+// Every kernel launch of the library is followed by QTT_CHECK_LAUNCH(), which
+// also counts it (qtt_launch_count() in the C ABI).
+void note_launch();
+#define QTT_CHECK_LAUNCH()  \
+  do {                      \
+    ::qtt::note_launch();   \
+    QTT_CUDA(cudaGetLastError()); \
+  } while (0)
 
 #define QTT_TRY(expr)                    \
   do {                                   \
@@ -77,6 +86,16 @@ struct GemmArgs {
 };
 
 int gemm(const GemmArgs& g, cudaStream_t stream);
+
+// Optional per-launch GEMM timing (CUDA events on the launching stream) used
+// by bench.py to report the DMMA kernel's achieved FLOP rate.
+struct GemmProfile {
+  bool on = false;
+  double flops = 0.0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
+  std::vector<double> launch_flops;
+};
+GemmProfile& gemm_profile();
 
 // Convenience: single column-major GEMM.
 inline int dgemm(cudaStream_t s, int ta, int tb, int m, int n, int k, double alpha,

@@ -31,7 +31,7 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 }
 
 template <int TA, int TB>
-__global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt) {
+__global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int kchunk, double* ws) {
   __shared__ double As[2][BK][BM + PAD];
   __shared__ double Bs[2][BK][BN + PAD];
 
@@ -42,7 +42,9 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt) {
   const double* A = g.a + bz * g.stride_a;
   const double* B = g.b + bz * g.stride_b;
   double* C = g.c + bz * g.stride_c;
-  const int M = g.m, N = g.n, K = g.k;
+  const int M = g.m, N = g.n;
+  const int kbeg = blockIdx.z * kchunk;
+  const int K = min(g.k, kbeg + kchunk);  // tiles cover [kbeg, K)
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
 
@@ -76,12 +78,12 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  const int ktiles = (K + BK - 1) / BK;
-  if (ktiles > 0) load_tile(0, 0);
+  const int ktiles = (K - kbeg + BK - 1) / BK;
+  if (ktiles > 0) load_tile(0, kbeg);
   for (int kt = 0; kt < ktiles; ++kt) {
     const int buf = kt & 1;
     if (kt + 1 < ktiles) {
-      load_tile(buf ^ 1, (kt + 1) * BK);
+      load_tile(buf ^ 1, kbeg + (kt + 1) * BK);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -103,6 +105,23 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt) {
     __syncthreads();
   }
 
+  if (ws != nullptr) {
+    // split-K partial: plain accumulator into ws[(z * batch + b) * M * N]
+    double* W = ws + ((int64_t)blockIdx.z * gridDim.y + bz) * (int64_t)M * N;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = m0 + wm + i * 8 + (lane >> 2);
+      if (row >= M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = n0 + wn + j * 8 + 2 * (lane & 3) + h;
+          if (col < N) W[row + (int64_t)col * M] = acc[i][j][h];
+        }
+    }
+    return;
+  }
   const double alpha = g.alpha, beta = g.beta;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -121,6 +140,23 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt) {
         }
       }
     }
+  }
+}
+
+__global__ void splitk_reduce_kernel(GemmArgs g, int splits, const double* __restrict__ ws) {
+  const int64_t mn = (int64_t)g.m * g.n;
+  const int64_t total = mn * g.batch;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / mn, e = i % mn;
+    const int r = (int)(e % g.m);
+    const int64_t c = e / g.m;
+    double acc = 0.0;
+    for (int s = 0; s < splits; ++s) acc += ws[((int64_t)s * g.batch + b) * mn + e];
+    double* p = g.c + b * g.stride_c + r + c * g.ldc;
+    double v = g.alpha * acc;
+    if (g.beta != 0.0) v += g.beta * *p;
+    *p = v;
   }
 }
 
@@ -171,6 +207,11 @@ __global__ void copy_matrix_kernel(int rows, int cols, const double* __restrict_
 
 }  // namespace
 
+GemmProfile& gemm_profile() {
+  static GemmProfile p;
+  return p;
+}
+
 int gemm(const GemmArgs& g, cudaStream_t stream) {
   if (g.m < 0 || g.n < 0 || g.k < 0 || g.batch < 0) return kInvalid;
   if (g.m == 0 || g.n == 0 || g.batch == 0) return kOk;
@@ -185,11 +226,47 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
   const int64_t tiles = (int64_t)mt * ceil_div(g.n, BN);
   if (tiles > 0x7fffffff) return kUnsupported;
   dim3 grid((unsigned)tiles, g.batch);
-  if (!g.trans_a && !g.trans_b) gemm_kernel<0, 0><<<grid, THREADS, 0, stream>>>(g, mt);
-  else if (!g.trans_a && g.trans_b) gemm_kernel<0, 1><<<grid, THREADS, 0, stream>>>(g, mt);
-  else if (g.trans_a && !g.trans_b) gemm_kernel<1, 0><<<grid, THREADS, 0, stream>>>(g, mt);
-  else gemm_kernel<1, 1><<<grid, THREADS, 0, stream>>>(g, mt);
+  GemmProfile& prof = gemm_profile();
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (prof.on) {
+    QTT_CUDA(cudaEventCreate(&e0));
+    QTT_CUDA(cudaEventCreate(&e1));
+    QTT_CUDA(cudaEventRecord(e0, stream));
+  }
+  // Split K when the tile grid cannot fill the SMs (skinny outputs with a
+  // long reduction, e.g. V^T A in the compact-WY updates); the partial sums
+  // are reduced in a fixed order, so results stay deterministic.
+  int splits = 1;
+  const int64_t ctas = tiles * g.batch;
+  if (ctas < num_sms() && g.k >= 512) {
+    splits = (int)std::min<int64_t>({16, ceil_div(2 * num_sms(), ctas), g.k / 256});
+    splits = std::max(splits, 1);
+  }
+  const int kchunk = splits > 1 ? (int)(ceil_div(ceil_div(g.k, splits), BK) * BK) : g.k;
+  if (splits > 1) splits = (int)ceil_div(g.k, kchunk);
+  double* ws = nullptr;
+  if (splits > 1)
+    QTT_CUDA(cudaMallocAsync(&ws, sizeof(double) * splits * g.batch * (int64_t)g.m * g.n, stream));
+  grid.z = splits;
+  if (!g.trans_a && !g.trans_b) gemm_kernel<0, 0><<<grid, THREADS, 0, stream>>>(g, mt, kchunk, ws);
+  else if (!g.trans_a && g.trans_b) gemm_kernel<0, 1><<<grid, THREADS, 0, stream>>>(g, mt, kchunk, ws);
+  else if (g.trans_a && !g.trans_b) gemm_kernel<1, 0><<<grid, THREADS, 0, stream>>>(g, mt, kchunk, ws);
+  else gemm_kernel<1, 1><<<grid, THREADS, 0, stream>>>(g, mt, kchunk, ws);
   QTT_CHECK_LAUNCH();
+  if (splits > 1) {
+    const int64_t total = (int64_t)g.m * g.n * g.batch;
+    const int blocks = (int)std::min<int64_t>(ceil_div(total, 256), 16 * num_sms());
+    splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(g, splits, ws);
+    QTT_CHECK_LAUNCH();
+    QTT_CUDA(cudaFreeAsync(ws, stream));
+  }
+  if (prof.on) {
+    QTT_CUDA(cudaEventRecord(e1, stream));
+    prof.events.emplace_back(e0, e1);
+    const double f = 2.0 * g.m * (double)g.n * g.k * g.batch;
+    prof.launch_flops.push_back(f);
+    prof.flops += f;
+  }
   return kOk;
 }
 

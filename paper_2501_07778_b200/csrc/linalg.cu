@@ -15,7 +15,7 @@ constexpr double kEps = 2.220446049250313e-16;
 
 // ------------------------------------------------------------------ panel QR
 constexpr int PNB = 32;          // panel width
-constexpr int PTHREADS = 256;    // 8 warps per CTA
+constexpr int PTHREADS = 512;    // 16 warps per CTA
 constexpr int PMAXROWS = 736;    // panel rows held per CTA (736*32*8 B = 184 KB)
 constexpr int PMAXCLUSTER = 16;  // non-portable cluster size (B200: 16 SMs per cluster)
 
@@ -32,19 +32,12 @@ struct PanelArgs {
   double* tau;
 };
 
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  // PTHREADS-thread reduction; returns the total to every thread.
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  v = warp_sum(v);
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double t = 0.0;
-#pragma unroll
-  for (int w = 0; w < PTHREADS / 32; ++w) t += red[w];
-  return t;
-}
-
+// One cluster reduction per column: every CTA publishes, for its rows
+// g > j, the partial dot products S_c = sum_g A[g,j] A[g,c] (c >= j, so
+// S_j is the squared norm) and the owner of row j publishes A[j, c].  With
+// v = (x - beta e_j) / (alpha - beta) the reflector's dots follow without a
+// second reduction: w_c = A[j,c] + scal * S_c.  Partials are double
+// buffered by column parity, so one cluster barrier per column suffices.
 __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
   extern __shared__ double smem[];
   cg::cluster_group cluster = cg::this_cluster();
@@ -55,41 +48,51 @@ __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
   const int nrows = max(0, min(pa.m - row0, pa.rpc));
   const int nb = pa.nb;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = PTHREADS / 32;
 
-  double* P = smem;                    // ld * PNB
-  double* partA = P + (size_t)ld * PNB;  // 2
-  double* partB = partA + 2;           // PNB
-  double* gram = partB + PNB;          // PNB*PNB (partial)
-  double* G = gram + PNB * PNB;        // PNB*PNB (total)
-  double* T = G + PNB * PNB;           // PNB*PNB
-  double* red = T + PNB * PNB;         // PTHREADS/32
-  double* tau_s = red + PTHREADS / 32; // PNB
+  double* P = smem;                          // ld * PNB
+  double* part = P + (size_t)ld * PNB;       // [2][2*PNB]
+  double* gS = part + 4 * PNB;               // PNB reduced S_c
+  double* gR = gS + PNB;                     // PNB row-j values
+  double* gram = gR + PNB;                   // PNB*PNB partial
+  double* G = gram + PNB * PNB;              // PNB*PNB total
+  double* T = G + PNB * PNB;                 // PNB*PNB
+  double* tau_s = T + PNB * PNB;             // PNB
 
   for (int idx = tid; idx < nrows * nb; idx += PTHREADS) {
     const int r = idx % nrows, c = idx / nrows;
     P[r + c * ld] = pa.A[(row0 + r) + (int64_t)c * pa.lda];
   }
+  const int jrow_local = -row0;  // local index of global row j is j - row0
   __syncthreads();
 
   for (int j = 0; j < nb; ++j) {
-    // ---- phase A: norm of the sub-diagonal part of column j
-    double sq = 0.0;
-    for (int r = tid; r < nrows; r += PTHREADS) {
-      if (row0 + r > j) {
-        const double x = P[r + j * ld];
-        sq = fma(x, x, sq);
-      }
+    double* pb = part + (j & 1) * 2 * PNB;
+    // (1) partial dots of column j with columns c >= j over local rows g > j
+    const int rstart = max(0, j + 1 - row0);
+    for (int c = j + warp; c < nb; c += NW) {
+      double acc = 0.0;
+      for (int r = rstart + lane; r < nrows; r += 32) acc = fma(P[r + j * ld], P[r + c * ld], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) pb[c] = acc;
     }
-    sq = block_sum(sq, red);
-    if (tid == 0) {
-      partA[0] = sq;
-      partA[1] = (j >= row0 && j < row0 + nrows) ? P[(j - row0) + j * ld] : 0.0;
-    }
+    const bool owner = (j >= row0 && j < row0 + nrows);
+    if (owner)
+      for (int c = j + tid; c < nb; c += PTHREADS) pb[PNB + c] = P[(j + jrow_local) + c * ld];
     cluster.sync();
-    double norm2 = 0.0;
-    for (int c = 0; c < cs; ++c) norm2 += cluster.map_shared_rank(partA, c)[0];
-    const int owner = min(j / pa.rpc, cs - 1);
-    const double alpha = cluster.map_shared_rank(partA, owner)[1];
+    // (2) gather the cluster-wide sums (independent DSMEM loads)
+    const int own_rank = min(j / pa.rpc, cs - 1);
+    for (int c = j + tid; c < nb; c += PTHREADS) {
+      double sum = 0.0;
+#pragma unroll 4
+      for (int q = 0; q < cs; ++q) sum += cluster.map_shared_rank(pb, q)[c];
+      gS[c] = sum;
+      gR[c] = cluster.map_shared_rank(pb, own_rank)[PNB + c];
+    }
+    __syncthreads();
+    // (3) reflector and rank-1 update of the local rows
+    const double norm2 = gS[j];
+    const double alpha = gR[j];
     double tau = 0.0, beta = alpha, scal = 1.0;
     if (norm2 > 0.0) {
       const double nrm = sqrt(fma(alpha, alpha, norm2));
@@ -97,60 +100,48 @@ __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
       tau = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
-    for (int r = tid; r < nrows; r += PTHREADS) {
-      const int g = row0 + r;
-      if (g > j) P[r + j * ld] *= scal;
-      else if (g == j) P[r + j * ld] = beta;
-    }
     if (tid == 0) tau_s[j] = tau;
-    __syncthreads();
-    // ---- phase B: w_c = v^T A[:, c] for the remaining panel columns
-    for (int c = j + 1 + warp; c < nb; c += PTHREADS / 32) {
-      double w = 0.0;
-      for (int r = lane; r < nrows; r += 32) {
-        const int g = row0 + r;
-        if (g >= j) {
-          const double v = (g == j) ? 1.0 : P[r + j * ld];
-          w = fma(v, P[r + c * ld], w);
-        }
-      }
-      w = warp_sum(w);
-      if (lane == 0) partB[c] = w;
-    }
-    cluster.sync();
     if (tau != 0.0) {
-      for (int c = j + 1; c < nb; ++c) {
-        double w = 0.0;
-        for (int q = 0; q < cs; ++q) w += cluster.map_shared_rank(partB, q)[c];
-        const double tw = tau * w;
-        for (int r = tid; r < nrows; r += PTHREADS) {
-          const int g = row0 + r;
-          if (g >= j) {
-            const double v = (g == j) ? 1.0 : P[r + j * ld];
-            P[r + c * ld] = fma(-tw, v, P[r + c * ld]);
-          }
+      for (int r = rstart + tid; r < nrows; r += PTHREADS) {
+        const double v = P[r + j * ld] * scal;
+        for (int c = j + 1; c < nb; ++c) {
+          const double w = fma(scal, gS[c], gR[c]);
+          P[r + c * ld] = fma(-tau * w, v, P[r + c * ld]);
+        }
+        P[r + j * ld] = v;
+      }
+      if (owner && tid == 0) {
+        const int r = j + jrow_local;
+        for (int c = j + 1; c < nb; ++c) {
+          const double w = fma(scal, gS[c], gR[c]);
+          P[r + c * ld] -= tau * w;
         }
       }
     }
+    if (owner && tid == 0) P[(j + jrow_local) + j * ld] = beta;
     __syncthreads();
   }
 
   // ---- Gram of V for the compact-WY T factor (dlarft, forward, columnwise)
-  for (int pq = tid; pq < nb * nb; pq += PTHREADS) {
+  for (int pq = warp; pq < nb * nb; pq += NW) {
     const int p = pq % nb, q = pq / nb;
+    if (q < p) continue;
     double acc = 0.0;
-    for (int r = 0; r < nrows; ++r) {
+    for (int r = lane; r < nrows; r += 32) {
       const int g = row0 + r;
       const double vp = (g == p) ? 1.0 : (g > p ? P[r + p * ld] : 0.0);
       const double vq = (g == q) ? 1.0 : (g > q ? P[r + q * ld] : 0.0);
       acc = fma(vp, vq, acc);
     }
-    gram[p + q * PNB] = acc;
+    acc = warp_sum(acc);
+    if (lane == 0) gram[p + q * PNB] = acc;
   }
   cluster.sync();
   for (int pq = tid; pq < nb * nb; pq += PTHREADS) {
     const int p = pq % nb, q = pq / nb;
+    if (q < p) continue;
     double acc = 0.0;
+#pragma unroll 4
     for (int c = 0; c < cs; ++c) acc += cluster.map_shared_rank(gram, c)[p + q * PNB];
     G[p + q * PNB] = acc;
   }
@@ -176,8 +167,9 @@ __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
     const int r = idx % nrows, q = idx / nrows;
     const int g = row0 + r;
     double y = 0.0, y2 = 0.0;
-    for (int p = 0; p < nb; ++p) {
-      const double v = (g == p) ? 1.0 : (g > p ? P[r + p * ld] : 0.0);
+    const int pmax = min(nb - 1, g);
+    for (int p = 0; p <= pmax; ++p) {
+      const double v = (g == p) ? 1.0 : P[r + p * ld];
       y = fma(v, T[q + p * PNB], y);
       y2 = fma(v, T[p + q * PNB], y2);
     }
@@ -191,7 +183,7 @@ __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
 }
 
 size_t panel_smem_bytes(int rpc) {
-  return sizeof(double) * ((size_t)rpc * PNB + 2 + PNB + 3 * PNB * PNB + PTHREADS / 32 + PNB);
+  return sizeof(double) * ((size_t)rpc * PNB + 4 * PNB + 2 * PNB + 3 * PNB * PNB + PNB);
 }
 
 int launch_panel(cudaStream_t s, const PanelArgs& pa0) {
@@ -220,6 +212,7 @@ int launch_panel(cudaStream_t s, const PanelArgs& pa0) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   QTT_CUDA(cudaLaunchKernelEx(&cfg, panel_qr_kernel, pa));
+  note_launch();
   return kOk;
 }
 
@@ -584,6 +577,7 @@ int jacobi(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int6
   void* args[] = {&p, &k, &X, &ldx, &W, &ldw, &tol_v, &flags};
   QTT_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_grid_kernel, dim3(blocks), dim3(256), args, 0,
                                        s));
+  note_launch();
   QTT_CUDA(cudaFreeAsync(flags, s));
   return kOk;
 }
