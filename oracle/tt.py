@@ -158,7 +158,7 @@ def _qr_sweep_right(cores):
         r, n, r2 = cores[k].shape
         q, rr = np.linalg.qr(cores[k].reshape(r, n * r2).T)
         cores[k] = np.ascontiguousarray(q.T).reshape(q.shape[1], n, r2)
-        cores[k - 1] = np.einsum("anb,cb->anc", cores[k - 1], rr)
+        cores[k - 1] = np.tensordot(cores[k - 1], rr.T, axes=(2, 0))
     return cores
 
 
@@ -169,7 +169,7 @@ def _svd_sweep_left(cores, delta):
         u, s, vt = np.linalg.svd(cores[k].reshape(r * n, r2), full_matrices=False)
         keep = min(chop(s, delta), cores[k + 1].shape[0])
         cores[k] = u[:, :keep].reshape(r, n, keep)
-        cores[k + 1] = np.einsum("ab,bnc->anc", s[:keep, None] * vt[:keep], cores[k + 1])
+        cores[k + 1] = np.tensordot(s[:keep, None] * vt[:keep], cores[k + 1], axes=(1, 0))
     return cores
 
 
@@ -177,7 +177,8 @@ def gram_norm(merged) -> float:
     """Norm by Gram accumulation (ttcore.py:341-347)."""
     g = np.ones((1, 1))
     for c in merged:
-        g = np.einsum("ab,anc,bnd->cd", g, c, c)
+        half = np.tensordot(g, c, axes=(1, 0))  # (a, n, d)
+        g = np.tensordot(c, half, axes=([0, 1], [0, 1]))
     return float(np.sqrt(max(g[0, 0], 0.0)))
 
 
@@ -201,7 +202,8 @@ def dot(a, b) -> float:
     """tt_dot (ttcore.py:355-363)."""
     g = np.ones((1, 1))
     for ca, cb in zip(a, b):
-        g = np.einsum("ab,anc,bnd->cd", g, ca, cb)
+        half = np.tensordot(g, cb, axes=(1, 0))
+        g = np.tensordot(ca, half, axes=([0, 1], [0, 1]))
     return float(g[0, 0])
 
 
