@@ -142,6 +142,21 @@ int qtt_zorder_dof_permutation(int32_t d, int64_t* perm, void* stream);
 int qtt_z_index(int32_t d, int64_t count, const int64_t* i, const int64_t* j,
                 int64_t* z, void* stream);
 
+/* ------------------------------------------------------------------ (a10)
+ * Element value grids, replaces element.element_stiffness_block /
+ * element_load_block (element.py:160-212) for all 16 corner pairs at once.
+ * coef: per Gauss point 25 doubles = J00[4], dJ10[4], dJ01[4] (entries
+ * x_xi, y_xi, x_eta, y_eta), weight, shape gradients [4][2], shape values
+ * [4]; cmat: 3x3 row-major C.  modulus (device, optional): [g][i][j]
+ * multiplier of the stiffness integrand (config-4 E(x,y) extension).
+ * kout: 64 vectors (pair a*4+b, component alpha*2+beta) and gout: 16
+ * vectors of length 4^d, zero-padded, in Z-order (zorder=1) or canonical
+ * order.  *degenerate = 1 if any |J| <= 0 (Python raises ValueError). */
+int qtt_element_grids(int32_t d, int32_t zorder, int32_t ngauss,
+                      const double* coef, const double* cmat,
+                      int32_t paper_det, const double* modulus, double* kout,
+                      double* gout, int32_t* degenerate, void* stream);
+
 /* ------------------------------------------------------ dense primitives
  * Exposed for the parity tests of the building blocks. */
 int qtt_gemm(int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,

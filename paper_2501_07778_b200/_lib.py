@@ -41,6 +41,7 @@ EXPORTS = (
     "qtt_zorder_permutation",
     "qtt_zorder_dof_permutation",
     "qtt_z_index",
+    "qtt_element_grids",
     "qtt_gemm",
     "qtt_qr",
     "qtt_svd",

@@ -295,7 +295,7 @@ int add(const qtt_layout* LA, const double* a, const qtt_layout* LB, const doubl
     sc.yr0 = (int)LB->ranks[l];
     sc.yr1 = (int)LB->ranks[l + 1];
     sc.sx = 1.0;
-    sc.sy = beta;
+    sc.sy = (l == 0) ? beta : 1.0;  // scaling the first core scales the TT
     sc.aux = sc.aux2 = 0;
   }
   return launch_struct(desc, a, b, c, s);
