@@ -157,6 +157,15 @@ int qtt_element_grids(int32_t d, int32_t zorder, int32_t ngauss,
                       int32_t paper_det, const double* modulus, double* kout,
                       double* gout, int32_t* degenerate, void* stream);
 
+/* ------------------------------------------------------------------ (a13)
+ * Dense local solve of the AMEn sweep, replaces np.linalg.solve in
+ * solver._solve_local (solver.py:162-173): blocked LU without pivoting on
+ * [M | b] with DMMA updates, residual check, Householder-QR fallback.
+ * M is n x n column-major (ldm); b, x have n entries (device).
+ * *fallback = 1 if the QR path was taken. */
+int qtt_dense_solve(int64_t n, const double* m, int64_t ldm, const double* b,
+                    double* x, int32_t* fallback, void* stream);
+
 /* ------------------------------------------------------ dense primitives
  * Exposed for the parity tests of the building blocks. */
 int qtt_gemm(int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,

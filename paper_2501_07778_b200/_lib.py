@@ -42,6 +42,7 @@ EXPORTS = (
     "qtt_zorder_dof_permutation",
     "qtt_z_index",
     "qtt_element_grids",
+    "qtt_dense_solve",
     "qtt_gemm",
     "qtt_qr",
     "qtt_svd",

@@ -1,0 +1,229 @@
+// Dense local solves of the AMEn sweep (row a13, K5c).
+//
+// The reference solves every local system with LAPACK dgesv
+// (solver.py:162-173).  Here: blocked right-looking LU without pivoting on
+// the augmented matrix [M | b] (64-wide diagonal blocks factorised and
+// inverted in shared memory, panel solves and the Schur update as DMMA
+// GEMMs), blocked back substitution, and a residual check.  The AMEn local
+// operators are Galerkin projections of a (nearly) symmetric positive
+// definite stiffness onto orthonormal bases, for which elimination without
+// pivoting is stable; if the residual check fails (tiny pivot or growth),
+// the solve falls back to Householder QR (backward stable, ~2x the flops).
+#include "../../include/qtt_b200.h"
+#include <cmath>
+
+#include "linalg.cuh"
+
+namespace qtt {
+namespace {
+
+constexpr int LB = 64;
+constexpr int kLuSmem = 2 * LB * (LB + 1) * sizeof(double);
+
+// Factor the kb x kb diagonal block in place (L unit lower, U upper) and
+// write L^{-1} and U^{-1} (LB x LB, zero padded) to linv / uinv.
+__global__ void __launch_bounds__(256) lu_diag_kernel(int kb, double* __restrict__ A, int64_t lda,
+                                                      double* __restrict__ linv,
+                                                      double* __restrict__ uinv,
+                                                      int* __restrict__ bad) {
+  extern __shared__ double lu_sm[];
+  double (*S)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(lu_sm);
+  double (*X)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(lu_sm + LB * (LB + 1));
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < LB * LB; idx += blockDim.x) {
+    const int r = idx % LB, c = idx / LB;
+    S[r][c] = (r < kb && c < kb) ? A[r + (int64_t)c * lda] : (r == c ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  for (int j = 0; j < kb; ++j) {
+    const double piv = S[j][j];
+    if (tid == 0 && !(fabs(piv) > 0.0)) atomicExch(bad, 1);
+    __syncthreads();
+    const double inv = 1.0 / piv;
+    for (int r = j + 1 + tid; r < kb; r += blockDim.x) S[r][j] *= inv;
+    __syncthreads();
+    const int rem = kb - j - 1;
+    for (int idx = tid; idx < rem * rem; idx += blockDim.x) {
+      const int r = j + 1 + idx % rem, c = j + 1 + idx / rem;
+      S[r][c] = fma(-S[r][j], S[j][c], S[r][c]);
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
+    const int r = idx % kb, c = idx / kb;
+    A[r + (int64_t)c * lda] = S[r][c];
+  }
+  // U^{-1}: column c by back substitution (thread c)
+  if (tid < LB) {
+    const int c = tid;
+    for (int r = 0; r < LB; ++r) X[r][c] = 0.0;
+    X[c][c] = 1.0 / S[c][c];
+    for (int i = c - 1; i >= 0; --i) {
+      double acc = 0.0;
+      for (int l = i + 1; l <= c; ++l) acc = fma(S[i][l], X[l][c], acc);
+      X[i][c] = -acc / S[i][i];
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < LB * LB; idx += blockDim.x) uinv[idx] = X[idx % LB][idx / LB];
+  __syncthreads();
+  // L^{-1} (unit lower): column c by forward substitution
+  if (tid < LB) {
+    const int c = tid;
+    for (int r = 0; r < LB; ++r) X[r][c] = 0.0;
+    X[c][c] = 1.0;
+    for (int i = c + 1; i < LB; ++i) {
+      double acc = 0.0;
+      for (int l = c; l < i; ++l) acc = fma(S[i][l], X[l][c], acc);
+      X[i][c] = -acc;
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < LB * LB; idx += blockDim.x) linv[idx] = X[idx % LB][idx / LB];
+}
+
+__global__ void residual_norms_kernel(int n, const double* __restrict__ r,
+                                      const double* __restrict__ b, double* out) {
+  __shared__ double s1[32], s2[32];
+  double a = 0.0, c = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    a = fma(r[i], r[i], a);
+    c = fma(b[i], b[i], c);
+  }
+  a = warp_sum(a);
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0) {
+    s1[threadIdx.x >> 5] = a;
+    s2[threadIdx.x >> 5] = c;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      x += s1[w];
+      y += s2[w];
+    }
+    out[0] = sqrt(x);
+    out[1] = sqrt(y);
+  }
+}
+
+}  // namespace
+
+// Solve M x = b (M: N x N column-major, ldm).  Returns kOk; *fallback
+// reports whether the QR path was needed.
+int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const double* b, double* x,
+                int* fallback) {
+  if (N <= 0) return kInvalid;
+  static bool configured = false;
+  if (!configured) {
+    QTT_CUDA(cudaFuncSetAttribute(lu_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLuSmem));
+    configured = true;
+  }
+  const int64_t ld = N;
+  const int nblk = (int)ceil_div(N, LB);
+  double *A, *linv, *uinv, *tmp, *r, *nrm;
+  int* bad;
+  QTT_CUDA(cudaMallocAsync(&A, sizeof(double) * ld * (N + 1), s));
+  QTT_CUDA(cudaMallocAsync(&linv, sizeof(double) * LB * LB * nblk, s));
+  QTT_CUDA(cudaMallocAsync(&uinv, sizeof(double) * LB * LB * nblk, s));
+  const int64_t tmp_elems = std::max<int64_t>({ld * LB, (int64_t)LB * (N + 1), (int64_t)LB * LB});
+  QTT_CUDA(cudaMallocAsync(&tmp, sizeof(double) * tmp_elems, s));
+  QTT_CUDA(cudaMallocAsync(&r, sizeof(double) * (N + 2), s));
+  QTT_CUDA(cudaMallocAsync(&bad, sizeof(int), s));
+  nrm = r + N;
+  QTT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  QTT_TRY(copy_matrix(s, N, N, M, ldm, A, ld));
+  QTT_CUDA(cudaMemcpyAsync(A + ld * N, b, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+  // ---- forward elimination on [M | b]
+  for (int kb0 = 0, blk = 0; kb0 < N; kb0 += LB, ++blk) {
+    const int kb = std::min(LB, N - kb0);
+    double* A11 = A + kb0 + (int64_t)kb0 * ld;
+    lu_diag_kernel<<<1, 256, kLuSmem, s>>>(kb, A11, ld, linv + (int64_t)blk * LB * LB,
+                                     uinv + (int64_t)blk * LB * LB, bad);
+    QTT_CHECK_LAUNCH();
+    const int m2 = N - kb0 - kb;      // rows below
+    const int n2 = N + 1 - kb0 - kb;  // columns right (incl. rhs)
+    if (m2 > 0) {
+      // L21 = A21 U11^{-1}
+      double* A21 = A + (kb0 + kb) + (int64_t)kb0 * ld;
+      QTT_TRY(dgemm(s, 0, 0, m2, kb, kb, 1.0, A21, ld, uinv + (int64_t)blk * LB * LB, LB, 0.0, tmp,
+                    m2));
+      QTT_TRY(copy_matrix(s, m2, kb, tmp, m2, A21, ld));
+    }
+    if (n2 > 0) {
+      // U12 = L11^{-1} A12 (includes the rhs column)
+      double* A12 = A + kb0 + (int64_t)(kb0 + kb) * ld;
+      QTT_TRY(dgemm(s, 0, 0, kb, n2, kb, 1.0, linv + (int64_t)blk * LB * LB, LB, A12, ld, 0.0, tmp,
+                    kb));
+      QTT_TRY(copy_matrix(s, kb, n2, tmp, kb, A12, ld));
+      if (m2 > 0) {
+        double* A21 = A + (kb0 + kb) + (int64_t)kb0 * ld;
+        double* A22 = A + (kb0 + kb) + (int64_t)(kb0 + kb) * ld;
+        QTT_TRY(dgemm(s, 0, 0, m2, n2, kb, -1.0, A21, ld, A12, ld, 1.0, A22, ld));
+      }
+    }
+  }
+  // ---- back substitution U x = y (y = last column)
+  double* y = A + ld * N;
+  for (int blk = nblk - 1; blk >= 0; --blk) {
+    const int kb0 = blk * LB;
+    const int kb = std::min(LB, N - kb0);
+    // x_k = U_kk^{-1} y_k
+    QTT_TRY(dgemm(s, 0, 0, kb, 1, kb, 1.0, uinv + (int64_t)blk * LB * LB, LB, y + kb0, N, 0.0,
+                  x + kb0, N));
+    if (kb0 > 0)  // y_{<k} -= U_{<k,k} x_k
+      QTT_TRY(dgemm(s, 0, 0, kb0, 1, kb, -1.0, A + (int64_t)kb0 * ld, ld, x + kb0, N, 1.0, y, N));
+  }
+  // ---- residual check with the original matrix
+  QTT_CUDA(cudaMemcpyAsync(r, b, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+  QTT_TRY(dgemm(s, 0, 0, N, 1, N, -1.0, M, ldm, x, N, 1.0, r, N));
+  residual_norms_kernel<<<1, 1024, 0, s>>>(N, r, b, nrm);
+  QTT_CHECK_LAUNCH();
+  double hn[2];
+  int hbad = 0;
+  QTT_CUDA(cudaMemcpyAsync(hn, nrm, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
+  QTT_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  QTT_CUDA(cudaStreamSynchronize(s));
+  const bool ok = !hbad && std::isfinite(hn[0]) && hn[0] <= 1e-10 * std::max(hn[1], 1e-300);
+  *fallback = ok ? 0 : 1;
+  if (!ok) {
+    // Householder QR: M = Q R, x = R^{-1} Q^T b (back substitution as above).
+    double *Q, *R;
+    QTT_CUDA(cudaMallocAsync(&Q, sizeof(double) * ld * N, s));
+    QTT_CUDA(cudaMallocAsync(&R, sizeof(double) * ld * N, s));
+    QTT_TRY(qr(s, N, N, M, ldm, Q, ld, R, ld));
+    QTT_TRY(dgemm(s, 1, 0, N, 1, N, 1.0, Q, ld, b, N, 0.0, y, N));
+    for (int blk = nblk - 1; blk >= 0; --blk) {
+      const int kb0 = blk * LB;
+      const int kb = std::min(LB, N - kb0);
+      // invert the diagonal block of R through the LU kernel (L = I)
+      QTT_TRY(copy_matrix(s, kb, kb, R + kb0 + (int64_t)kb0 * ld, ld, tmp, LB));
+      lu_diag_kernel<<<1, 256, kLuSmem, s>>>(kb, tmp, LB, linv, uinv, bad);
+      QTT_CHECK_LAUNCH();
+      QTT_TRY(dgemm(s, 0, 0, kb, 1, kb, 1.0, uinv, LB, y + kb0, N, 0.0, x + kb0, N));
+      if (kb0 > 0)
+        QTT_TRY(dgemm(s, 0, 0, kb0, 1, kb, -1.0, R + (int64_t)kb0 * ld, ld, x + kb0, N, 1.0, y, N));
+    }
+    QTT_CUDA(cudaFreeAsync(Q, s));
+    QTT_CUDA(cudaFreeAsync(R, s));
+  }
+  QTT_CUDA(cudaFreeAsync(A, s));
+  QTT_CUDA(cudaFreeAsync(linv, s));
+  QTT_CUDA(cudaFreeAsync(uinv, s));
+  QTT_CUDA(cudaFreeAsync(tmp, s));
+  QTT_CUDA(cudaFreeAsync(r, s));
+  QTT_CUDA(cudaFreeAsync(bad, s));
+  return kOk;
+}
+
+}  // namespace qtt
+
+extern "C" int qtt_dense_solve(int64_t n, const double* m, int64_t ldm, const double* b, double* x,
+                               int32_t* fallback, void* stream) {
+  if (n < 1 || n > 0x7fffffff || !fallback) return QTT_EINVAL;
+  int fb = 0;
+  int st = qtt::dense_solve(reinterpret_cast<cudaStream_t>(stream), (int)n, m, ldm, b, x, &fb);
+  *fallback = fb;
+  return st;
+}

@@ -1,19 +1,79 @@
-"""AMEn-style TT solve on the device: drop-in for ``qttfem.solver``."""
+"""AMEn-style TT solve of K u = f on the device: drop-in for ``qttfem.solver``
+(solver.py:21-426).
+
+Same algorithm and control flow as the reference: one-site ALS sweeps with
+residual-projection enrichment by a rank-``enrichment_rank`` companion
+(forward half-sweep), SVD truncation at
+delta = trunc_factor * eps * adapt * ||x_d|| / sqrt(d) (backward half-sweep),
+relative residual after every sweep, stall adaptation, final compression.
+Every contraction runs on the DMMA GEMM of libqttb200.so, local systems are
+solved by the device LU (``qtt_dense_solve``), QR/SVD by the device
+Householder / Jacobi kernels.  The only data that reaches the host per sweep
+are the scalars that steer control flow (residual, truncation ranks).
+
+Initial cores come from numpy ``default_rng(seed)`` exactly as in the
+reference (solver.py:258-261, 419-426) and are uploaded.
+"""
 
 from __future__ import annotations
 
 import ctypes
+import time
+from dataclasses import dataclass
 
 import numpy as np
 import torch
 
 from . import _lib
-from .ttcore import TTMatrix, TTVector, tt_contract_device, tt_norm
+from ._dense import dense_solve_colmajor, mm, qr_colmajor, svd_left_colmajor
+from .ttcore import (
+    TTMatrix,
+    TTVector,
+    _concat,
+    tt_contract_device,
+    tt_matvec,
+    tt_norm,
+    tt_round,
+    tt_sub,
+)
 
 __all__ = ["SolverConfig", "SolveOutcome", "solve", "residual", "apply_tt_matrix"]
 
-_DENSE_LOCAL_LIMIT = 1200
-_DENSE_RESIDUAL_BITS = 22
+_DENSE_LOCAL_LIMIT = 1200  # kept for API parity (solver.py:23); local solves are direct
+_DENSE_RESIDUAL_BITS = 22  # materialise vectors up to 2^22 entries (solver.py:24)
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    epsilon: float = 1e-8
+    max_sweeps: int = 40
+    enrichment_rank: int = 4
+    local_solver: str = "auto"  # direct | iterative | auto  (all use the device LU)
+    seed: int = 0
+    trunc_factor: float = 0.5
+    max_rank: int = 400
+
+    def __post_init__(self):
+        if self.epsilon <= 0:
+            raise ValueError("epsilon must be positive")
+        if self.max_sweeps < 1:
+            raise ValueError("max_sweeps must be >= 1")
+        if self.local_solver not in ("auto", "direct", "iterative"):
+            raise ValueError(f"unknown local solver {self.local_solver!r}")
+
+
+@dataclass(frozen=True)
+class SolveOutcome:
+    u: TTVector
+    residual: float
+    sweeps: int
+    rank_history: tuple
+    residual_history: tuple
+    wall_time: float
+    converged: bool
+
+
+# ------------------------------------------------------------- residual
 
 
 def apply_tt_matrix(A: TTMatrix, v) -> torch.Tensor:
@@ -26,3 +86,293 @@ def apply_tt_matrix(A: TTMatrix, v) -> torch.Tensor:
     _lib.call("qtt_dense_apply", ctypes.byref(lay), _lib.ptr(A.data), _lib.ptr(x), _lib.ptr(out),
               _lib.stream_handle())
     return out
+
+
+def residual(K: TTMatrix, u: TTVector, f: TTVector, rounding_eps=None) -> float:
+    """||K u - f|| / ||f|| (solver.py:81-103).  Dense on the device up to
+    2^_DENSE_RESIDUAL_BITS entries, else in TT arithmetic with the norm taken
+    after orthogonalisation (no sqrt(eps) floor)."""
+    fn = tt_norm(f)
+    if fn == 0.0:
+        return 0.0
+    if len(u.cores) <= _DENSE_RESIDUAL_BITS:
+        ud = tt_contract_device(u)
+        fd = tt_contract_device(f)
+        r = apply_tt_matrix(K, ud) - fd
+        return float(torch.linalg.vector_norm(r) / torch.linalg.vector_norm(fd))
+    y = tt_sub(tt_matvec(K, u), f)
+    if rounding_eps is not None:
+        y = tt_round(y, rounding_eps / 100.0)
+    return tt_norm(y) / fn
+
+
+# ------------------------------------------------- interface contractions
+
+
+def _phi_left(phi, xrow, a_p, xcol):
+    """(x,a,y),(x,i,X),A,(y,j,Y) -> (X,b,Y)   (solver.py:109-112)."""
+    x, a, y = phi.shape
+    _, n, X = xrow.shape
+    Y = xcol.shape[2]
+    b = a_p["rb"]
+    t1 = mm(phi.reshape(x, a * y), xrow.reshape(x, n * X), ta=True)  # (a,y,i,X)
+    t1 = t1.view(a, y, n, X).permute(1, 3, 0, 2).reshape(y * X, a * n)
+    t2 = mm(t1, a_p["ai_jb"])  # (y,X,j,b)
+    t2 = t2.view(y, X, n, b).permute(1, 3, 0, 2).reshape(X * b, y * n)
+    return mm(t2, xcol.reshape(y * n, Y)).view(X, b, Y)
+
+
+def _phi_right(phi, xrow, a_p, xcol):
+    """(X,b,Y),(x,i,X),A,(y,j,Y) -> (x,a,y)   (solver.py:115-118)."""
+    X, b, Y = phi.shape
+    x, n, _ = xrow.shape
+    y = xcol.shape[0]
+    a = a_p["ra"]
+    t1 = mm(xrow.reshape(x * n, X), phi.reshape(X, b * Y))  # (x,i,b,Y)
+    t1 = t1.view(x, n, b, Y).permute(0, 3, 1, 2).reshape(x * Y, n * b)
+    t2 = mm(t1, a_p["ib_aj"])  # (x,Y,a,j)
+    t2 = t2.view(x, Y, a, n).permute(0, 2, 1, 3).reshape(x * a, Y * n)
+    xc = xcol.permute(2, 1, 0).reshape(Y * n, y)
+    return mm(t2, xc).view(x, a, y)
+
+
+def _psi_left(psi, xrow, f):
+    """(x,q),(x,i,X),(q,i,p) -> (X,p)   (solver.py:121-123)."""
+    x, q = psi.shape
+    _, n, X = xrow.shape
+    t = mm(psi, xrow.reshape(x, n * X), ta=True)  # (q,i,X)
+    return mm(t.view(q * n, X), f.reshape(q * n, f.shape[2]), ta=True)
+
+
+def _psi_right(psi, xrow, f):
+    """(X,p),(x,i,X),(q,i,p) -> (x,q)   (solver.py:126-128)."""
+    x, n, X = xrow.shape
+    t = mm(xrow.reshape(x * n, X), psi)  # (x,i,p)
+    return mm(t.view(x, n * psi.shape[1]), f.reshape(f.shape[0], n * f.shape[2]), tb=True)
+
+
+def _local_rhs(psi_l, f, psi_r):
+    """(x,q),(q,i,p),(g,p) -> (x,i,g)   (solver.py:131-133)."""
+    x, q = psi_l.shape
+    _, n, p = f.shape
+    t = mm(psi_l, f.reshape(q, n * p))
+    return mm(t.view(x * n, p), psi_r, tb=True).view(x, n, psi_r.shape[0])
+
+
+def _local_matrix_cm(phi_l, a_p, phi_r):
+    """Column-major local operator M[(x,i,g),(y,j,h)] (solver.py:148-152):
+    memory laid out as the C-order tensor (y,j,h,x,i,g)."""
+    x, a, y = phi_l.shape
+    g, b, h = phi_r.shape
+    n = a_p["n"]
+    pl = phi_l.permute(0, 2, 1).reshape(x * y, a)
+    t = mm(pl, a_p["a_ijb"])  # (x,y,i,j,b)
+    pr = phi_r.permute(1, 0, 2).reshape(b, g * h)
+    mat = mm(t.view(x * y * n * n, b), pr)  # (x,y,i,j,g,h)
+    mat = mat.view(x, y, n, n, g, h).permute(1, 3, 5, 0, 2, 4).contiguous()
+    return mat.view(-1)
+
+
+def _solve_local(phi_l, a_p, phi_r, rhs):
+    rl, n, rr = rhs.shape
+    dim = rl * n * rr
+    mcm = _local_matrix_cm(phi_l, a_p, phi_r)
+    sol, _ = dense_solve_colmajor(mcm, dim, rhs.reshape(-1))
+    return sol.view(rl, n, rr)
+
+
+def _proj_a(zl, xk, a_p, zr):
+    """einsum zaL,LjR,aijb,ZbR -> ziZ (solver.py:306-313, 318-323)."""
+    z, a, L = zl.shape
+    _, n, R = xk.shape
+    Z, b, _ = zr.shape
+    t = mm(zl.reshape(z * a, L), xk.reshape(L, n * R))  # (z,a,j,R)
+    t = t.view(z, a, n, R).permute(0, 3, 1, 2).reshape(z * R, a * n)
+    t2 = mm(t, a_p["aj_ib"])  # (z,R,i,b)
+    t2 = t2.view(z, R, n, b).permute(0, 2, 3, 1).reshape(z * n, b * R)
+    return mm(t2, zr.reshape(Z, b * R), tb=True).view(z, n, Z)
+
+
+# ---------------------------------------------------------- QR and SVD
+
+
+def _qr_core_left(core):
+    rl, n, rr = core.shape
+    cm = core.reshape(rl * n, rr).t().contiguous()  # column-major (rl n x rr)
+    q, r, k = qr_colmajor(cm, rl * n, rr)
+    qc = q.view(k, rl * n).t().contiguous().view(rl, n, k)
+    rc = r.view(rr, k).t().contiguous()  # (k, rr)
+    return qc, rc
+
+
+def _qr_core_right(core):
+    rl, n, rr = core.shape
+    q, r, k = qr_colmajor(core.contiguous().view(-1), n * rr, rl)
+    return q.view(k, n, rr), r.view(rl, k)  # q^T core, R^T (rl x k)
+
+
+def _truncated_split_right(core, delta, rmax):
+    """Right factor V_r^T and left carry U_r s_r (solver.py:221-236)."""
+    rl, n, rr = core.shape
+    s, v, k = svd_left_colmajor(core.contiguous().view(-1), n * rr, rl)  # left vectors of M^T
+    sh = s.cpu().numpy()
+    tail = np.sqrt(np.cumsum(sh[::-1] ** 2))[::-1]
+    above = np.nonzero(tail > delta)[0]
+    r = int(above[-1] + 1) if above.size else 1
+    r = max(1, min(r, rmax))
+    vr = v[: (n * rr) * r].view(r, n, rr)  # V[:, :r] column-major == C-order (r, n, rr)
+    carry = mm(core.reshape(rl, n * rr), vr.reshape(r, n * rr), tb=True)  # M V_r = U_r s_r
+    return vr.contiguous(), carry
+
+
+def _safe_core(core, rng):
+    if float(torch.linalg.vector_norm(core)) == 0.0:
+        return torch.from_numpy(np.asarray(rng.standard_normal(tuple(core.shape))) * 1e-30).to(core.device)
+    return core
+
+
+def _right_orthogonalize_all(cores):
+    cores = list(cores)
+    for k in range(len(cores) - 1, 0, -1):
+        cores[k], carry = _qr_core_right(cores[k])
+        cl = cores[k - 1]
+        r0, n, r1 = cl.shape
+        cores[k - 1] = mm(cl.reshape(r0 * n, r1), carry).view(r0, n, carry.shape[1])
+    return cores
+
+
+def _init_cores(rng, sizes, rank, dev):
+    d = len(sizes)
+    ranks = [1] + [rank] * (d - 1) + [1]
+    host = [rng.standard_normal((ranks[k], sizes[k], ranks[k + 1])) for k in range(d)]
+    return _right_orthogonalize_all([torch.from_numpy(c).to(dev) for c in host])
+
+
+def _operator_views(K: TTMatrix):
+    """Per-core permuted copies of the operator cores used by the GEMMs."""
+    views = []
+    for c in K.cores:
+        ra, n, m, rb = c.shape
+        views.append({
+            "ra": ra, "rb": rb, "n": n,
+            "a_ijb": c.reshape(ra, n * m * rb),
+            "ai_jb": c.reshape(ra * n, m * rb),
+            "ib_aj": c.permute(1, 3, 0, 2).reshape(n * rb, ra * m).contiguous(),
+            "aj_ib": c.permute(0, 2, 1, 3).reshape(ra * m, n * rb).contiguous(),
+        })
+    return views
+
+
+# ------------------------------------------------------------------ solve
+
+
+def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig) -> SolveOutcome:
+    """AMEn-style alternating solve of K u = f (solver.py:239-389)."""
+    if K.col_mode_sizes != f.mode_sizes or K.row_mode_sizes != f.mode_sizes:
+        raise ValueError("operator and right-hand side modes do not match")
+    t0 = time.perf_counter()
+    dev = _lib.device()
+    fnorm = tt_norm(f)
+    d = f.d
+    sizes = f.mode_sizes
+    if fnorm == 0.0:
+        zero = TTVector([np.zeros((1, n, 1)) for n in sizes])
+        return SolveOutcome(zero, 0.0, 0, (1,), (0.0,), time.perf_counter() - t0, True)
+
+    rng = np.random.default_rng(cfg.seed)
+    rho = cfg.enrichment_rank
+    x = _init_cores(rng, sizes, 2, dev)
+    z = _init_cores(rng, sizes, rho, dev)
+    A = _operator_views(K)
+    F = [c.contiguous() for c in f.cores]
+
+    one3 = torch.ones((1, 1, 1), dtype=torch.float64, device=dev)
+    one2 = torch.ones((1, 1), dtype=torch.float64, device=dev)
+    phi_r = [None] * (d + 1)
+    psi_r = [None] * (d + 1)
+    za_r = [None] * (d + 1)
+    zf_r = [None] * (d + 1)
+    phi_r[d], psi_r[d], za_r[d], zf_r[d] = one3, one2, one3, one2
+    for k in range(d - 1, -1, -1):
+        phi_r[k] = _phi_right(phi_r[k + 1], x[k], A[k], x[k])
+        psi_r[k] = _psi_right(psi_r[k + 1], x[k], F[k])
+        za_r[k] = _phi_right(za_r[k + 1], z[k], A[k], x[k])
+        zf_r[k] = _psi_right(zf_r[k + 1], z[k], F[k])
+    phi_l = [None] * (d + 1)
+    psi_l = [None] * (d + 1)
+    za_l = [None] * (d + 1)
+    zf_l = [None] * (d + 1)
+    phi_l[0], psi_l[0], za_l[0], zf_l[0] = one3, one2, one3, one2
+
+    rank_history, residual_history = [], []
+    res, res_prev = np.inf, np.inf
+    adapt = 1.0
+    sweeps_done = 0
+    for sweep in range(cfg.max_sweeps):
+        # ---------------- forward: solve + enrich ----------------
+        for k in range(d):
+            rhs = _local_rhs(psi_l[k], F[k], psi_r[k + 1])
+            xk = _solve_local(phi_l[k], A[k], phi_r[k + 1], rhs)
+            x[k] = xk
+            if k < d - 1:
+                zrhs = _local_rhs(zf_l[k], F[k], zf_r[k + 1])
+                zloc = zrhs - _proj_a(za_l[k], xk, A[k], za_r[k + 1])
+                z[k], _ = _qr_core_left(_safe_core(zloc, rng))
+                wrhs = _local_rhs(psi_l[k], F[k], zf_r[k + 1])
+                w = wrhs - _proj_a(phi_l[k], xk, A[k], za_r[k + 1])
+                xe = torch.cat([x[k], w], dim=2)
+                nxt = x[k + 1]
+                nxt = torch.cat([nxt, torch.zeros((w.shape[2],) + tuple(nxt.shape[1:]), dtype=torch.float64,
+                                                  device=dev)], dim=0)
+                x[k], carry = _qr_core_left(xe)
+                r0, n1, r2 = nxt.shape
+                x[k + 1] = mm(carry, nxt.reshape(r0, n1 * r2)).view(carry.shape[0], n1, r2)
+                phi_l[k + 1] = _phi_left(phi_l[k], x[k], A[k], x[k])
+                psi_l[k + 1] = _psi_left(psi_l[k], x[k], F[k])
+                za_l[k + 1] = _phi_left(za_l[k], z[k], A[k], x[k])
+                zf_l[k + 1] = _psi_left(zf_l[k], z[k], F[k])
+        # ---------------- backward: solve + truncate ----------------
+        xnorm = float(torch.linalg.vector_norm(x[d - 1]))
+        delta = cfg.trunc_factor * cfg.epsilon * adapt * max(xnorm, 1e-300) / np.sqrt(d)
+        for k in range(d - 1, -1, -1):
+            rhs = _local_rhs(psi_l[k], F[k], psi_r[k + 1])
+            xk = _solve_local(phi_l[k], A[k], phi_r[k + 1], rhs)
+            if k > 0:
+                x[k], carry = _truncated_split_right(xk, delta, cfg.max_rank)
+                p0, pn, p1 = x[k - 1].shape
+                x[k - 1] = mm(x[k - 1].reshape(p0 * pn, p1), carry).view(p0, pn, carry.shape[1])
+                phi_r[k] = _phi_right(phi_r[k + 1], x[k], A[k], x[k])
+                psi_r[k] = _psi_right(psi_r[k + 1], x[k], F[k])
+                z[k], _ = _qr_core_right(_safe_core(z[k], rng))
+                za_r[k] = _phi_right(za_r[k + 1], z[k], A[k], x[k])
+                zf_r[k] = _psi_right(zf_r[k + 1], z[k], F[k])
+            else:
+                x[k] = xk
+        sweeps_done = sweep + 1
+        rank_history.append(max(c.shape[0] for c in x[1:]) if d > 1 else 1)
+        u = _concat(TTVector, x)
+        res = residual(K, u, f)
+        residual_history.append(float(res))
+        if res <= cfg.epsilon:
+            break
+        if res > 0.7 * res_prev and adapt > 2.0**-44:
+            adapt *= 0.25
+        res_prev = res
+
+    u = _concat(TTVector, x)
+    if res <= cfg.epsilon:
+        u, res = _final_compress(K, f, u, res, cfg.epsilon)
+    return SolveOutcome(u, float(res), sweeps_done, tuple(rank_history), tuple(residual_history),
+                        time.perf_counter() - t0, bool(res <= cfg.epsilon))
+
+
+def _final_compress(K, f, u, res, epsilon):
+    """Loosest re-rounding that keeps the residual within epsilon (solver.py:392-409)."""
+    if max(epsilon - res, 0.0) <= 0.0:
+        return u, res
+    for factor in (0.5, 0.25, 0.1, 0.03, 0.01, 0.003):
+        cand = tt_round(u, factor * epsilon)
+        r = residual(K, cand, f)
+        if r <= epsilon:
+            return cand, r
+    return u, res

@@ -1,0 +1,129 @@
+"""Device AMEn solve (rows a13, a14) against the reference's golden solutions."""
+
+import os
+
+import numpy as np
+import pytest
+
+from tests.golden import cases
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(name):
+    return np.load(os.path.join(GOLD, f"{name}.npz"))
+
+
+def mesh_of(spec):
+    from paper_2501_07778_b200.mesh import SubdomainMesh
+
+    return SubdomainMesh(np.asarray(spec["corners"]), spec["d"], dict(spec.get("tags", {})),
+                         dict(spec.get("tractions", {})))
+
+
+def global_system(name):
+    from paper_2501_07778_b200 import assembly as A
+    from paper_2501_07778_b200 import coupling as C
+    from paper_2501_07778_b200.material import MaterialModel
+    from paper_2501_07778_b200.topology import DomainTopology
+
+    spec = cases.coupling_cases()[name]
+    meshes = [mesh_of(s) for s in spec["meshes"]]
+    topo = DomainTopology.from_subdomains(meshes)
+    mat = MaterialModel(*spec["material"])
+    systems = [A.assemble_subdomain(m, mat, "zorder", spec["eps"], body_force=spec["body"]) for m in meshes]
+    return C.apply_dirichlet(C.concat_blocks(systems, topo, ordering="zorder", epsilon=spec["eps"]),
+                             epsilon=spec["eps"]), spec
+
+
+@pytest.mark.parametrize("name", ["single3", "lshape2", "cantilever2"])
+def test_solve_matches_reference(name):
+    from paper_2501_07778_b200 import solver as S
+    from paper_2501_07778_b200.ttcore import tt_contract
+
+    g = load("coupling")
+    gsys, spec = global_system(name)
+    eps = spec["solve"]
+    out = S.solve(gsys.K, gsys.f, S.SolverConfig(epsilon=eps, seed=0, local_solver="direct"))
+    assert out.converged
+    assert out.residual <= eps
+    kd, fd = g[f"{name}_Kd"], g[f"{name}_fd"]
+    u_exact = np.linalg.solve(kd, fd)
+    u_ref = g[f"{name}_u"]
+    u_gpu = tt_contract(out.u)
+    ref_err = np.linalg.norm(u_ref - u_exact) / np.linalg.norm(u_exact)
+    gpu_err = np.linalg.norm(u_gpu - u_exact) / np.linalg.norm(u_exact)
+    cond = np.linalg.cond(kd)
+    assert gpu_err <= max(10 * ref_err, cond * eps) + 1e-10, (gpu_err, ref_err)
+    # residual evaluated on the reference's own dense operator
+    assert np.linalg.norm(kd @ u_gpu - fd) / np.linalg.norm(fd) <= eps * (1 + 1e-6)
+
+
+def test_identity_solve_and_zero_rhs():
+    from paper_2501_07778_b200 import solver as S
+    from paper_2501_07778_b200 import ttcore as T
+
+    rng = np.random.default_rng(3)
+    sizes = (2,) * 5
+    rk = [1, 3, 3, 3, 3, 1]
+    f = T.TTVector([rng.standard_normal((rk[k], 2, rk[k + 1])) for k in range(5)])
+    out = S.solve(T.tt_identity(sizes), f, S.SolverConfig(epsilon=1e-10, seed=7))
+    assert out.converged and out.sweeps <= 1
+    assert np.allclose(T.tt_contract(out.u), T.tt_contract(f), atol=1e-9)
+    z = T.TTVector([np.zeros((1, 2, 1))] * 4)
+    out = S.solve(T.tt_identity((2,) * 4), z, S.SolverConfig(epsilon=1e-8))
+    assert out.converged and out.residual == 0.0
+    with pytest.raises(ValueError):
+        S.solve(T.tt_identity((2, 2)), T.TTVector([np.ones((1, 2, 1))] * 3), S.SolverConfig(epsilon=1e-6))
+
+
+def test_residual_tt_path_matches_dense():
+    from paper_2501_07778_b200 import solver as S
+    from paper_2501_07778_b200 import ttcore as T
+
+    gsys, _ = global_system("cantilever2")
+    rng = np.random.default_rng(2)
+    sizes = gsys.f.mode_sizes
+    rk = [1] + [2] * (len(sizes) - 1) + [1]
+    u = T.TTVector([rng.standard_normal((rk[k], sizes[k], rk[k + 1])) for k in range(len(sizes))])
+    dense = S.residual(gsys.K, u, gsys.f)
+    old = S._DENSE_RESIDUAL_BITS
+    try:
+        S._DENSE_RESIDUAL_BITS = 0
+        tt = S.residual(gsys.K, u, gsys.f)
+    finally:
+        S._DENSE_RESIDUAL_BITS = old
+    assert np.isclose(tt, dense, rtol=1e-10)
+
+
+def test_determinism():
+    from paper_2501_07778_b200 import solver as S
+
+    gsys, _ = global_system("cantilever2")
+    cfg = S.SolverConfig(epsilon=1e-6, seed=42)
+    a = S.solve(gsys.K, gsys.f, cfg)
+    b = S.solve(gsys.K, gsys.f, cfg)
+    assert a.rank_history == b.rank_history
+    assert a.residual == b.residual
+    for ca, cb in zip(a.u.cores, b.u.cores):
+        assert bool((ca == cb).all())
+
+
+def test_dense_solve_kernel():
+    import torch
+
+    from paper_2501_07778_b200._dense import dense_solve_colmajor
+
+    rng = np.random.default_rng(11)
+    for n in (5, 64, 130, 700):
+        a = rng.standard_normal((n, n))
+        m = a @ a.T + n * np.eye(n)
+        b = rng.standard_normal(n)
+        x, fb = dense_solve_colmajor(torch.tensor(m.T.ravel(), device="cuda"), n, torch.tensor(b, device="cuda"))
+        assert np.linalg.norm(m @ x.cpu().numpy() - b) <= 1e-11 * np.linalg.norm(b)
+    # a matrix that needs pivoting falls back to QR
+    m = np.array([[0.0, 1.0], [1.0, 0.0]])
+    x, fb = dense_solve_colmajor(torch.tensor(m.T.ravel(), device="cuda"), 2, torch.tensor([1.0, 2.0], dtype=torch.float64, device="cuda"))
+    assert fb and np.allclose(x.cpu().numpy(), [2.0, 1.0])
