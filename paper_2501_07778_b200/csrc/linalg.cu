@@ -4,6 +4,8 @@
 // occur.  See linalg.cuh for the contracts.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "linalg.cuh"
 
 namespace cg = cooperative_groups;
@@ -51,8 +53,8 @@ __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
   constexpr int NW = PTHREADS / 32;
 
   double* P = smem;                          // ld * PNB
-  double* part = P + (size_t)ld * PNB;       // [2][2*PNB]
-  double* gS = part + 4 * PNB;               // PNB reduced S_c
+  double* part = P + (size_t)ld * PNB;       // [2][PMAXCLUSTER + 1][PNB] pushed partials
+  double* gS = part + 2 * (PMAXCLUSTER + 1) * PNB;  // PNB reduced S_c
   double* gR = gS + PNB;                     // PNB row-j values
   double* gram = gR + PNB;                   // PNB*PNB partial
   double* G = gram + PNB * PNB;              // PNB*PNB total
@@ -67,27 +69,29 @@ __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
   __syncthreads();
 
   for (int j = 0; j < nb; ++j) {
-    double* pb = part + (j & 1) * 2 * PNB;
-    // (1) partial dots of column j with columns c >= j over local rows g > j
+    double* pb = part + (j & 1) * (PMAXCLUSTER + 1) * PNB;
+    // (1) partial dots of column j with columns c >= j over local rows g > j,
+    //     pushed into slot [crank] of every CTA (remote stores do not stall)
     const int rstart = max(0, j + 1 - row0);
     for (int c = j + warp; c < nb; c += NW) {
       double acc = 0.0;
       for (int r = rstart + lane; r < nrows; r += 32) acc = fma(P[r + j * ld], P[r + c * ld], acc);
       acc = warp_sum(acc);
-      if (lane == 0) pb[c] = acc;
+      if (lane < cs) cluster.map_shared_rank(pb, lane)[crank * PNB + c] = acc;
     }
     const bool owner = (j >= row0 && j < row0 + nrows);
     if (owner)
-      for (int c = j + tid; c < nb; c += PTHREADS) pb[PNB + c] = P[(j + jrow_local) + c * ld];
+      for (int idx = tid; idx < (nb - j) * cs; idx += PTHREADS) {
+        const int c = j + idx % (nb - j), q = idx / (nb - j);
+        cluster.map_shared_rank(pb, q)[PMAXCLUSTER * PNB + c] = P[(j + jrow_local) + c * ld];
+      }
     cluster.sync();
-    // (2) gather the cluster-wide sums (independent DSMEM loads)
-    const int own_rank = min(j / pa.rpc, cs - 1);
+    // (2) reduce the pushed partials locally (same order in every CTA)
     for (int c = j + tid; c < nb; c += PTHREADS) {
       double sum = 0.0;
-#pragma unroll 4
-      for (int q = 0; q < cs; ++q) sum += cluster.map_shared_rank(pb, q)[c];
+      for (int q = 0; q < cs; ++q) sum += pb[q * PNB + c];
       gS[c] = sum;
-      gR[c] = cluster.map_shared_rank(pb, own_rank)[PNB + c];
+      gR[c] = pb[PMAXCLUSTER * PNB + c];
     }
     __syncthreads();
     // (3) reflector and rank-1 update of the local rows
@@ -183,7 +187,8 @@ __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
 }
 
 size_t panel_smem_bytes(int rpc) {
-  return sizeof(double) * ((size_t)rpc * PNB + 4 * PNB + 2 * PNB + 3 * PNB * PNB + PNB);
+  return sizeof(double) *
+         ((size_t)rpc * PNB + 2 * (PMAXCLUSTER + 1) * PNB + 2 * PNB + 3 * PNB * PNB + PNB);
 }
 
 int launch_panel(cudaStream_t s, const PanelArgs& pa0) {
@@ -254,7 +259,7 @@ __device__ __forceinline__ void rr_pair(int kp, int r, int q, int& i, int& j) {
 
 // One Jacobi rotation on columns (i, j) by one warp; returns 1 if rotated.
 __device__ int jacobi_pair(double* X, int64_t ldx, double* W, int64_t ldw, int p, int k, int i,
-                           int j, double tol) {
+                           int j, double tol, double noise2) {
   const int lane = threadIdx.x & 31;
   double a = 0.0, b = 0.0, g = 0.0;
   double* xi = X + (int64_t)i * ldx;
@@ -268,7 +273,9 @@ __device__ int jacobi_pair(double* X, int64_t ldx, double* W, int64_t ldw, int p
   a = warp_sum(a);
   b = warp_sum(b);
   g = warp_sum(g);
-  if (g == 0.0 || !(fabs(g) > tol * sqrt(a) * sqrt(b))) return 0;
+  // Columns below the noise level eps*||X||_F sit far under the _chop floor
+  // (s0 * max(k,2) * eps); rotating them only churns rounding noise.
+  if (g == 0.0 || a < noise2 || b < noise2 || !(fabs(g) > tol * sqrt(a) * sqrt(b))) return 0;
   const double zeta = (b - a) / (2.0 * g);
   const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
   const double c = 1.0 / sqrt(fma(t, t, 1.0));
@@ -289,6 +296,7 @@ __device__ int jacobi_pair(double* X, int64_t ldx, double* W, int64_t ldw, int p
 }
 
 constexpr int JMAXSWEEPS = 60;
+__device__ int g_jacobi_sweeps;  // sweeps used by the last Jacobi launch (diagnostics)
 constexpr int JTHREADS = 1024;
 
 // Small problems: one CTA, X and W staged in shared memory.
@@ -305,6 +313,22 @@ __global__ void __launch_bounds__(JTHREADS) jacobi_smem_kernel(int p, int k, dou
     Ws[idx] = ((idx % k) == (idx / k)) ? 1.0 : 0.0;
   const int kp = k + (k & 1);
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ double red[32];
+  __shared__ double noise2;
+  {
+    double acc = 0.0;
+    for (int idx = threadIdx.x; idx < p * k; idx += blockDim.x) acc = fma(Xs[idx], Xs[idx], acc);
+    acc = warp_sum(acc);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < nw; ++w) t += red[w];
+      noise2 = t * kEps * kEps;
+    }
+    __syncthreads();
+  }
   for (int sweep = 0; sweep < JMAXSWEEPS; ++sweep) {
     if (threadIdx.x == 0) rotated = 0;
     __syncthreads();
@@ -313,12 +337,13 @@ __global__ void __launch_bounds__(JTHREADS) jacobi_smem_kernel(int p, int k, dou
       for (int q = warp; q < kp / 2; q += nw) {
         int i, j;
         rr_pair(kp, r, q, i, j);
-        if (j < k) any |= jacobi_pair(Xs, p, Ws, k, p, k, i, j, tol);
+        if (j < k) any |= jacobi_pair(Xs, p, Ws, k, p, k, i, j, tol, noise2);
       }
       __syncthreads();
     }
     if (any && (threadIdx.x & 31) == 0) rotated = 1;
     __syncthreads();
+    if (threadIdx.x == 0) g_jacobi_sweeps = sweep + 1;
     if (!rotated) break;
     __syncthreads();
   }
@@ -326,6 +351,153 @@ __global__ void __launch_bounds__(JTHREADS) jacobi_smem_kernel(int p, int k, dou
     X[(idx % p) + (int64_t)(idx / p) * ldx] = Xs[idx];
   for (int idx = threadIdx.x; idx < k * k; idx += blockDim.x)
     W[(idx % k) + (int64_t)(idx / k) * ldw] = Ws[idx];
+}
+
+// Mid-size problems: a thread-block cluster holds X and W in distributed
+// shared memory, ROWS spread over the CTAs.  Per round every CTA computes the
+// partial (alpha, beta, gamma) of all k/2 disjoint pairs over its rows, one
+// cluster barrier publishes them, every CTA reduces the same partials in the
+// same order (so all CTAs take identical rotation decisions) and rotates its
+// own rows.  Partials are double buffered by round parity: one cluster
+// barrier per round.
+constexpr int JC_THREADS = 512;
+
+__global__ void __launch_bounds__(JC_THREADS) jacobi_cluster_kernel(int p, int k, double* X,
+                                                                     int64_t ldx, double* W,
+                                                                     int64_t ldw, double tol,
+                                                                     int px, int pw) {
+  extern __shared__ double jc[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cs = (int)cluster.num_blocks();
+  const int cr = (int)cluster.block_rank();
+  const int kp = k + (k & 1);
+  const int np = kp / 2;
+  const int x0 = cr * px, nx = max(0, min(p - x0, px));
+  const int w0 = cr * pw, nw = max(0, min(k - w0, pw));
+  double* Xs = jc;                        // px x kp (column-major, ld px)
+  double* Ws = Xs + (size_t)px * kp;      // pw x kp
+  double* part = Ws + (size_t)pw * kp;    // [2][cs][np][3], pushed by every CTA
+  double* rot = part + 2 * 3 * np * cs;   // [np][2] (c, s); c = 2 marks "no rotation"
+  __shared__ int any_rot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NWARP = JC_THREADS / 32;
+  for (int idx = tid; idx < px * kp; idx += JC_THREADS) {
+    const int r = idx % px, c = idx / px;
+    Xs[idx] = (r < nx && c < k) ? X[(x0 + r) + (int64_t)c * ldx] : 0.0;
+  }
+  for (int idx = tid; idx < pw * kp; idx += JC_THREADS) {
+    const int r = idx % pw, c = idx / pw;
+    Ws[idx] = (r < nw && c < k) ? ((w0 + r) == c ? 1.0 : 0.0) : 0.0;
+  }
+  __syncthreads();
+  // ||X||_F^2: every CTA pushes its partial into slot [cr] of every CTA
+  double* np2 = rot + 2 * np;  // [cs]
+  {
+    double acc = 0.0;
+    for (int idx = tid; idx < px * kp; idx += JC_THREADS) acc = fma(Xs[idx], Xs[idx], acc);
+    acc = warp_sum(acc);
+    __shared__ double red[JC_THREADS / 32];
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (tid < cs) {
+      double t = 0.0;
+      for (int w = 0; w < NWARP; ++w) t += red[w];
+      cluster.map_shared_rank(np2, tid)[cr] = t;
+    }
+  }
+  cluster.sync();
+  double noise2 = 0.0;
+  for (int c = 0; c < cs; ++c) noise2 += np2[c];
+  noise2 *= kEps * kEps;
+  int round_no = 0;
+  for (int sweep = 0; sweep < JMAXSWEEPS; ++sweep) {
+    if (tid == 0) any_rot = 0;
+    for (int r = 0; r < kp - 1; ++r, ++round_no) {
+      double* pb = part + (size_t)(round_no & 1) * 3 * np * cs;
+      for (int q = warp; q < np; q += NWARP) {
+        int i, j;
+        rr_pair(kp, r, q, i, j);
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int rr = lane; rr < nx; rr += 32) {
+          const double u = Xs[rr + i * px], v = Xs[rr + j * px];
+          a = fma(u, u, a);
+          b = fma(v, v, b);
+          g = fma(u, v, g);
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        g = warp_sum(g);
+        // push this CTA's partials into slot [cr] of every CTA (remote
+        // stores do not stall; the cluster barrier orders them)
+        if (lane < cs) {
+          double* dst = cluster.map_shared_rank(pb, lane) + 3 * ((size_t)cr * np + q);
+          dst[0] = a;
+          dst[1] = b;
+          dst[2] = g;
+        }
+      }
+      cluster.sync();
+      for (int q = tid; q < np; q += JC_THREADS) {
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int c = 0; c < cs; ++c) {
+          const double* rp = pb + 3 * ((size_t)c * np + q);
+          a += rp[0];
+          b += rp[1];
+          g += rp[2];
+        }
+        int i, j;
+        rr_pair(kp, r, q, i, j);
+        double cc = 2.0, sn = 0.0;
+        if (j < k && g != 0.0 && a >= noise2 && b >= noise2 && fabs(g) > tol * sqrt(a) * sqrt(b)) {
+          const double zeta = (b - a) / (2.0 * g);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          cc = 1.0 / sqrt(fma(t, t, 1.0));
+          sn = cc * t;
+          any_rot = 1;
+        }
+        rot[2 * q] = cc;
+        rot[2 * q + 1] = sn;
+      }
+      __syncthreads();
+      // rotate local rows of X and W
+      const int totx = np * nx, totw = np * nw;
+      for (int idx = tid; idx < totx + totw; idx += JC_THREADS) {
+        const bool isx = idx < totx;
+        const int e = isx ? idx : idx - totx;
+        const int nr = isx ? nx : nw;
+        const int q = e / nr, rr = e % nr;
+        const double cc = rot[2 * q];
+        if (cc == 2.0) continue;
+        const double sn = rot[2 * q + 1];
+        int i, j;
+        rr_pair(kp, r, q, i, j);
+        double* base = isx ? Xs : Ws;
+        const int ld = isx ? px : pw;
+        const double u = base[rr + i * ld], v = base[rr + j * ld];
+        base[rr + i * ld] = cc * u - sn * v;
+        base[rr + j * ld] = sn * u + cc * v;
+      }
+      __syncthreads();
+    }
+    const int done = !any_rot;
+    __syncthreads();
+    if (cr == 0 && tid == 0) g_jacobi_sweeps = sweep + 1;
+    if (done) break;
+  }
+  cluster.sync();  // no CTA exits while others may read its partials
+  for (int idx = tid; idx < nx * k; idx += JC_THREADS) {
+    const int r = idx % nx, c = idx / nx;
+    X[(x0 + r) + (int64_t)c * ldx] = Xs[r + c * px];
+  }
+  for (int idx = tid; idx < nw * k; idx += JC_THREADS) {
+    const int r = idx % nw, c = idx / nw;
+    W[(w0 + r) + (int64_t)c * ldw] = Ws[r + c * pw];
+  }
+}
+
+size_t jacobi_cluster_smem(int px, int pw, int k, int cs) {
+  const int kp = k + (k & 1);
+  return sizeof(double) * ((size_t)(px + pw) * kp + 3 * (size_t)kp * cs + kp + 16);
 }
 
 // Large problems: cooperative grid, columns stay in global memory (L2).
@@ -342,7 +514,7 @@ __global__ void __launch_bounds__(256) jacobi_grid_kernel(int p, int k, double* 
       for (int q = gw; q < kp / 2; q += nw) {
         int i, j;
         rr_pair(kp, r, q, i, j);
-        if (j < k) any |= jacobi_pair(X, ldx, W, ldw, p, k, i, j, tol);
+        if (j < k) any |= jacobi_pair(X, ldx, W, ldw, p, k, i, j, tol, 0.0);
       }
       grid.sync();
     }
@@ -548,7 +720,30 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
   return kOk;
 }
 
+static int jacobi_impl(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw);
+
 int jacobi(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw) {
+  static const bool dbg = getenv("QTT_JACOBI_DEBUG") != nullptr;
+  cudaEvent_t e0, e1;
+  if (dbg) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+  }
+  const int st = jacobi_impl(s, p, k, X, ldx, W, ldw);
+  if (dbg) {
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    int sw = 0;
+    cudaMemcpyFromSymbol(&sw, g_jacobi_sweeps, sizeof(int));
+    fprintf(stderr, "[jacobi] p=%d k=%d sweeps=%d ms=%.3f\n", p, k, sw, ms);
+  }
+  return st;
+}
+
+static int jacobi_impl(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw) {
   if (p <= 0 || k <= 0) return kInvalid;
   const double tol = sqrt((double)std::max(p, 1)) * kEps;
   const size_t smem = sizeof(double) * ((size_t)p * k + (size_t)k * k);
@@ -562,6 +757,35 @@ int jacobi(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int6
     const int threads = std::min(JTHREADS, std::max(32, ((k + 1) / 2) * 32));
     jacobi_smem_kernel<<<1, threads, smem, s>>>(p, k, X, ldx, W, ldw, tol);
     QTT_CHECK_LAUNCH();
+    return kOk;
+  }
+  // cluster path: smallest cluster whose per-CTA slice fits 200 KB
+  for (int cs = 2; cs <= 16; ++cs) {
+    const int px = (int)ceil_div(p, cs), pw = (int)ceil_div(k, cs);
+    const size_t bytes = jacobi_cluster_smem(px, pw, k, cs);
+    if (bytes > 200 * 1024) continue;
+    static bool cconf = false;
+    if (!cconf) {
+      QTT_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      QTT_CUDA(cudaFuncSetAttribute(jacobi_cluster_kernel,
+                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cconf = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs, 1, 1);
+    cfg.blockDim = dim3(JC_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    QTT_CUDA(cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel, p, k, X, ldx, W, ldw, tol, px, pw));
+    note_launch();
     return kOk;
   }
   QTT_TRY(set_identity(s, k, k, W, ldw));
