@@ -30,6 +30,11 @@ def config(idx: int, d: int | None = None):
         mesh = SubdomainMesh(UNIT, d, {"left": "clamped"}, {"right": (1.0, 0.0)})
         mat = MaterialModel(1.0, 0.3, "plane-stress", modulus_field=config4_modulus)
         return [mesh], mat, (0.0, 0.0), EPS
+    if idx == 40:
+        # SURVEY's "config-4-like" probe: config 4 with a constant E = 1
+        d = 10 if d is None else d
+        mesh = SubdomainMesh(UNIT, d, {"left": "clamped"}, {"right": (1.0, 0.0)})
+        return [mesh], MaterialModel(1.0, 0.3, "plane-stress"), (0.0, 0.0), EPS
     if idx == 5:
         d = 10 if d is None else d
         meshes = [
