@@ -15,7 +15,7 @@ struct MatPerm {
   int n[QTT_MAX_CORES], m[QTT_MAX_CORES];
 };
 
-__global__ void merged_to_dense_kernel(MatPerm mp, int64_t rows, int64_t total,
+__global__ void merged_to_dense_kernel(const __grid_constant__ MatPerm mp, int64_t rows, int64_t total,
                                        const double* __restrict__ merged, double* __restrict__ out) {
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
        g += (int64_t)gridDim.x * blockDim.x) {

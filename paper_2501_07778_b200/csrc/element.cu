@@ -39,7 +39,7 @@ __device__ __forceinline__ int64_t squeeze_bits(int64_t z, int d) {
 
 // grid (4 pair-groups): thread handles one output position and one corner a
 // (4 partner corners b, 4 components each + 4 load weights).
-__global__ void element_grids_kernel(ElemCoef ec, const double* __restrict__ modulus,
+__global__ void element_grids_kernel(const __grid_constant__ ElemCoef ec, const double* __restrict__ modulus,
                                      double* __restrict__ kout, double* __restrict__ gout,
                                      int* __restrict__ degenerate) {
   const int64_t npos = 1LL << (2 * ec.d);

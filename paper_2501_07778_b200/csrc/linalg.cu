@@ -34,12 +34,21 @@ struct PanelArgs {
   double* tau;
 };
 
-// One cluster reduction per column: every CTA publishes, for its rows
-// g > j, the partial dot products S_c = sum_g A[g,j] A[g,c] (c >= j, so
-// S_j is the squared norm) and the owner of row j publishes A[j, c].  With
-// v = (x - beta e_j) / (alpha - beta) the reflector's dots follow without a
-// second reduction: w_c = A[j,c] + scal * S_c.  Partials are double
-// buffered by column parity, so one cluster barrier per column suffices.
+// One cluster reduction per column.  For column j every CTA pushes, over
+// its rows g > j, the dots of column j with every panel column c:
+//   c >= j : S_c = sum_g A[g,j] A[g,c]      (S_j = squared norm)
+//   c <  j : Z_c = sum_g V[g,c] A[g,j]      (for the compact-WY T factor)
+// and the owner of row j pushes that row.  With v = (x - beta e_j)/(alpha - beta)
+// the reflector dots follow without a second reduction,
+//   w_c = A[j,c] + scal S_c,   (V^T v_j)_c = V[j,c] + scal Z_c,
+// so T (dlarft, forward, columnwise) is accumulated on the fly.  Partials are
+// double buffered by column parity: one cluster barrier per column and none
+// after the loop.
+__device__ __forceinline__ void panel_barrier(cg::cluster_group& cl, int cs) {
+  if (cs == 1) __syncthreads();
+  else cl.sync();
+}
+
 __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
   extern __shared__ double smem[];
   cg::cluster_group cluster = cg::this_cluster();
@@ -51,50 +60,55 @@ __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
   const int nb = pa.nb;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = PTHREADS / 32;
+  constexpr int SLOT = 2 * PNB;  // per-CTA slot: [dots (PNB) | owner row (PNB)]
 
-  double* P = smem;                          // ld * PNB
-  double* part = P + (size_t)ld * PNB;       // [2][PMAXCLUSTER + 1][PNB] pushed partials
-  double* gS = part + 2 * (PMAXCLUSTER + 1) * PNB;  // PNB reduced S_c
-  double* gR = gS + PNB;                     // PNB row-j values
-  double* gram = gR + PNB;                   // PNB*PNB partial
-  double* G = gram + PNB * PNB;              // PNB*PNB total
-  double* T = G + PNB * PNB;                 // PNB*PNB
-  double* tau_s = T + PNB * PNB;             // PNB
+  double* P = smem;                                // ld * PNB
+  double* part = P + (size_t)ld * PNB;             // [2][PMAXCLUSTER][SLOT]
+  double* gS = part + 2 * PMAXCLUSTER * SLOT;      // PNB reduced dots
+  double* gR = gS + PNB;                           // PNB row-j values
+  double* T = gR + PNB;                            // PNB*PNB
+  double* tau_s = T + PNB * PNB;                   // PNB
 
   for (int idx = tid; idx < nrows * nb; idx += PTHREADS) {
     const int r = idx % nrows, c = idx / nrows;
     P[r + c * ld] = pa.A[(row0 + r) + (int64_t)c * pa.lda];
   }
-  const int jrow_local = -row0;  // local index of global row j is j - row0
+  for (int idx = tid; idx < PNB * PNB; idx += PTHREADS) T[idx] = 0.0;
   __syncthreads();
 
   for (int j = 0; j < nb; ++j) {
-    double* pb = part + (j & 1) * (PMAXCLUSTER + 1) * PNB;
-    // (1) partial dots of column j with columns c >= j over local rows g > j,
-    //     pushed into slot [crank] of every CTA (remote stores do not stall)
+    double* pb = part + (j & 1) * PMAXCLUSTER * SLOT;
     const int rstart = max(0, j + 1 - row0);
-    for (int c = j + warp; c < nb; c += NW) {
+    // (1) dots of column j with all panel columns over local rows g > j
+    for (int c = warp; c < nb; c += NW) {
       double acc = 0.0;
       for (int r = rstart + lane; r < nrows; r += 32) acc = fma(P[r + j * ld], P[r + c * ld], acc);
       acc = warp_sum(acc);
-      if (lane < cs) cluster.map_shared_rank(pb, lane)[crank * PNB + c] = acc;
+      if (cs == 1) {
+        if (lane == 0) pb[c] = acc;
+      } else if (lane < cs) {
+        cluster.map_shared_rank(pb, lane)[crank * SLOT + c] = acc;
+      }
     }
     const bool owner = (j >= row0 && j < row0 + nrows);
-    if (owner)
-      for (int idx = tid; idx < (nb - j) * cs; idx += PTHREADS) {
-        const int c = j + idx % (nb - j), q = idx / (nb - j);
-        cluster.map_shared_rank(pb, q)[PMAXCLUSTER * PNB + c] = P[(j + jrow_local) + c * ld];
+    if (owner) {
+      const int rj = j - row0;
+      for (int idx = tid; idx < nb * cs; idx += PTHREADS) {
+        const int c = idx % nb, q = idx / nb;
+        double* dst = (cs == 1) ? pb : cluster.map_shared_rank(pb, q);
+        dst[PNB + c] = P[rj + c * ld];  // owner row lands in slot 0's row half
       }
-    cluster.sync();
-    // (2) reduce the pushed partials locally (same order in every CTA)
-    for (int c = j + tid; c < nb; c += PTHREADS) {
+    }
+    panel_barrier(cluster, cs);
+    // (2) local reduction of the pushed partials (same order everywhere)
+    for (int c = tid; c < nb; c += PTHREADS) {
       double sum = 0.0;
-      for (int q = 0; q < cs; ++q) sum += pb[q * PNB + c];
+      for (int q = 0; q < cs; ++q) sum += pb[q * SLOT + c];
       gS[c] = sum;
-      gR[c] = pb[PMAXCLUSTER * PNB + c];
+      gR[c] = pb[PNB + c];
     }
     __syncthreads();
-    // (3) reflector and rank-1 update of the local rows
+    // (3) reflector
     const double norm2 = gS[j];
     const double alpha = gR[j];
     double tau = 0.0, beta = alpha, scal = 1.0;
@@ -104,7 +118,18 @@ __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
       tau = (beta - alpha) / beta;
       scal = 1.0 / (alpha - beta);
     }
-    if (tid == 0) tau_s[j] = tau;
+    // (4) T column j (warp 0) while the other warps update the rows
+    if (warp == NW - 1) {
+      if (lane == 0) {
+        tau_s[j] = tau;
+        T[j + j * PNB] = tau;
+      }
+      if (lane < j) {
+        double acc = 0.0;
+        for (int l = lane; l < j; ++l) acc = fma(T[lane + l * PNB], fma(scal, gS[l], gR[l]), acc);
+        T[lane + j * PNB] = -tau * acc;
+      }
+    }
     if (tau != 0.0) {
       for (int r = rstart + tid; r < nrows; r += PTHREADS) {
         const double v = P[r + j * ld] * scal;
@@ -115,56 +140,13 @@ __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
         P[r + j * ld] = v;
       }
       if (owner && tid == 0) {
-        const int r = j + jrow_local;
-        for (int c = j + 1; c < nb; ++c) {
-          const double w = fma(scal, gS[c], gR[c]);
-          P[r + c * ld] -= tau * w;
-        }
+        const int rj = j - row0;
+        for (int c = j + 1; c < nb; ++c) P[rj + c * ld] -= tau * fma(scal, gS[c], gR[c]);
       }
     }
-    if (owner && tid == 0) P[(j + jrow_local) + j * ld] = beta;
+    if (owner && tid == 0) P[(j - row0) + j * ld] = beta;
     __syncthreads();
   }
-
-  // ---- Gram of V for the compact-WY T factor (dlarft, forward, columnwise)
-  for (int pq = warp; pq < nb * nb; pq += NW) {
-    const int p = pq % nb, q = pq / nb;
-    if (q < p) continue;
-    double acc = 0.0;
-    for (int r = lane; r < nrows; r += 32) {
-      const int g = row0 + r;
-      const double vp = (g == p) ? 1.0 : (g > p ? P[r + p * ld] : 0.0);
-      const double vq = (g == q) ? 1.0 : (g > q ? P[r + q * ld] : 0.0);
-      acc = fma(vp, vq, acc);
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) gram[p + q * PNB] = acc;
-  }
-  cluster.sync();
-  for (int pq = tid; pq < nb * nb; pq += PTHREADS) {
-    const int p = pq % nb, q = pq / nb;
-    if (q < p) continue;
-    double acc = 0.0;
-#pragma unroll 4
-    for (int c = 0; c < cs; ++c) acc += cluster.map_shared_rank(gram, c)[p + q * PNB];
-    G[p + q * PNB] = acc;
-  }
-  cluster.sync();  // remote gram reads done before any CTA may exit
-  if (warp == 0) {
-    for (int j = 0; j < nb; ++j) {
-      double tij = 0.0;
-      if (lane < j) {
-        for (int l = lane; l < j; ++l) tij = fma(T[lane + l * PNB], G[l + j * PNB], tij);
-        tij *= -tau_s[j];
-      }
-      __syncwarp();
-      if (lane < j) T[lane + j * PNB] = tij;
-      if (lane == j) T[j + j * PNB] = tau_s[j];
-      if (lane > j && lane < nb) T[lane + j * PNB] = 0.0;
-      __syncwarp();
-    }
-  }
-  __syncthreads();
 
   // ---- outputs: V (explicit), Y = V T^T, Y2 = V T, R rows, tau
   for (int idx = tid; idx < nrows * nb; idx += PTHREADS) {
@@ -188,7 +170,7 @@ __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
 
 size_t panel_smem_bytes(int rpc) {
   return sizeof(double) *
-         ((size_t)rpc * PNB + 2 * (PMAXCLUSTER + 1) * PNB + 2 * PNB + 3 * PNB * PNB + PNB);
+         ((size_t)rpc * PNB + 2 * PMAXCLUSTER * 2 * PNB + 2 * PNB + PNB * PNB + PNB);
 }
 
 int launch_panel(cudaStream_t s, const PanelArgs& pa0) {
@@ -201,7 +183,10 @@ int launch_panel(cudaStream_t s, const PanelArgs& pa0) {
     configured = true;
   }
   PanelArgs pa = pa0;
-  const int cs = (int)ceil_div(pa.m, PMAXROWS);
+  // spread tall panels over up to 16 CTAs (>= 256 rows each) so the
+  // per-column work per CTA stays small; single CTA below 384 rows.
+  int cs = (int)std::max<int64_t>(ceil_div(pa.m, PMAXROWS), std::min<int64_t>(16, pa.m / 256));
+  cs = std::max(cs, 1);
   if (cs > PMAXCLUSTER) return kUnsupported;
   pa.rpc = (int)ceil_div(pa.m, cs);
   cudaLaunchConfig_t cfg = {};

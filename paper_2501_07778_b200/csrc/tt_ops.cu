@@ -12,7 +12,7 @@
 namespace qtt {
 namespace {
 
-constexpr int kUnit = 4096;       // output elements per block
+
 constexpr int kProdThreads = 256;
 
 struct ProdCore {
@@ -29,60 +29,95 @@ struct ProdDesc {
   ProdCore c[QTT_MAX_CORES];
 };
 
-__device__ __forceinline__ double prod_elem(const ProdCore& pc, const double* __restrict__ A,
-                                            const double* __restrict__ B, int a, int c, int i,
-                                            int kk, int b, int e) {
-  if (pc.mode == 1) {
-    // hadamard: X[a, i, b] * Y[c, i, e]  (i is the merged mode)
-    return __ldg(A + ((int64_t)a * pc.n + i) * pc.ra1 + b) *
-           __ldg(B + ((int64_t)c * pc.n + i) * pc.rb1 + e);
-  }
-  double s = 0.0;
-  const double* ap = A + (((int64_t)a * pc.n + i) * pc.m) * pc.ra1 + b;
-  const double* bp = B + (((int64_t)c * pc.m) * pc.k + kk) * pc.rb1 + e;
-  for (int j = 0; j < pc.m; ++j)
-    s = fma(__ldg(ap + (int64_t)j * pc.ra1), __ldg(bp + (int64_t)j * pc.k * pc.rb1), s);
-  return s;
-}
-
 __device__ __forceinline__ void st_cs2(double* p, double x, double y) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(x), "d"(y) : "memory");
 }
 
-__global__ void __launch_bounds__(kProdThreads) core_product_kernel(ProdDesc desc,
+// Slab-structured product.  For fixed (c, i, kk) the output entries
+// y[(a,c), i, kk, (b,e)] = sum_j A[a,i,j,b] B[c,j,kk,e] form a "slab" of
+// ra0 rows.  One block per slab: the A slice A[:, i, :, :] is staged once in
+// shared memory (broadcast reads), every thread keeps its column pair
+// B[c, :, kk, e:e+2] in registers for the whole slab and loops over (a, b):
+// 2m FMAs and one 16-byte streaming store per iteration, no per-element
+// index arithmetic.  (mode 1 = hadamard: no j sum, B indexed by i.)
+constexpr int kSlabA = 4096;  // doubles of the staged A slice (32 KB)
+
+__global__ void __launch_bounds__(kProdThreads) core_product_kernel(const __grid_constant__ ProdDesc desc,
                                                                      const double* __restrict__ A,
                                                                      const double* __restrict__ B,
                                                                      double* __restrict__ C) {
+  __shared__ double As[kSlabA];
   for (int64_t u = blockIdx.x; u < desc.total_units; u += gridDim.x) {
     int ci = 0;
     while (ci + 1 < desc.ncores && desc.c[ci + 1].unit_begin <= u) ++ci;
     const ProdCore& pc = desc.c[ci];
-    const int64_t Q = (int64_t)pc.ra1 * pc.rb1;
-    const int64_t rows = (int64_t)pc.ra0 * pc.rb0 * pc.n * pc.k;
-    const int64_t total = rows * Q;
-    const int64_t start = (u - pc.unit_begin) * kUnit;
-    const int64_t stop = min(start + (int64_t)kUnit, total);
+    const int rb1 = pc.rb1, ra1 = pc.ra1, ra0 = pc.ra0;
+    const int m = pc.mode == 1 ? 1 : pc.m;
+    const int64_t slab = u - pc.unit_begin;  // (c, i, kk)
+    const int kk = (int)(slab % pc.k);
+    const int i = (int)((slab / pc.k) % pc.n);
+    const int cc = (int)(slab / ((int64_t)pc.k * pc.n));
+    const int64_t Q = (int64_t)ra1 * rb1;
     const double* a = A + pc.a_off;
-    const double* b = B + pc.b_off;
+    const double* bb = B + pc.b_off;
     double* c = C + pc.c_off;
-    for (int64_t f = start + 2 * threadIdx.x; f < stop; f += 2 * kProdThreads) {
-      double v[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t g = f + h;
-        if (g >= stop) { v[h] = 0.0; continue; }
-        const int64_t row = g / Q;
-        const int col = (int)(g - row * Q);
-        int64_t t = row;
-        const int kk = (int)(t % pc.k); t /= pc.k;
-        const int i = (int)(t % pc.n); t /= pc.n;
-        const int cc = (int)(t % pc.rb0);
-        const int aa = (int)(t / pc.rb0);
-        const int bb = col / pc.rb1, ee = col - bb * pc.rb1;
-        v[h] = prod_elem(pc, a, b, aa, cc, i, kk, bb, ee);
+    // stage A[:, i, :, :] as As[(aa * m + j) * ra1 + b]
+    const int aslice = ra0 * m * ra1;
+    const bool staged = aslice <= kSlabA;
+    __syncthreads();
+    if (staged) {
+      for (int t = threadIdx.x; t < aslice; t += kProdThreads) {
+        const int bq = t % ra1, rest = t / ra1, j = rest % m, aa = rest / m;
+        As[t] = pc.mode == 1 ? a[((int64_t)aa * pc.n + i) * ra1 + bq]
+                             : a[(((int64_t)aa * pc.n + i) * pc.m + j) * ra1 + bq];
       }
-      if (f + 1 < stop) st_cs2(c + f, v[0], v[1]);
-      else c[f] = v[0];
+    }
+    __syncthreads();
+    const int ep_count = (rb1 + 1) / 2;
+    const int ep_lanes = min(ep_count, kProdThreads);
+    const int b_lanes = kProdThreads / ep_lanes;
+    const int tid = threadIdx.x;
+    if (tid >= ep_lanes * b_lanes) continue;
+    const int ep0 = tid % ep_lanes, bl = tid / ep_lanes;
+    const bool aligned = ((rb1 & 1) == 0) && ((pc.c_off & 1) == 0);
+    for (int ep = ep0; ep < ep_count; ep += ep_lanes) {
+      const int e = 2 * ep;
+      const bool two = e + 1 < rb1;
+      double x0[4], x1[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        x0[j] = x1[j] = 0.0;
+        if (j < m) {
+          const double* bp = pc.mode == 1 ? bb + ((int64_t)cc * pc.n + i) * rb1 + e
+                                          : bb + (((int64_t)cc * pc.m + j) * pc.k + kk) * rb1 + e;
+          x0[j] = __ldg(bp);
+          x1[j] = two ? __ldg(bp + 1) : 0.0;
+        }
+      }
+      for (int aa = 0; aa < ra0; ++aa) {
+        const int64_t row = (((int64_t)aa * pc.rb0 + cc) * pc.n + i) * pc.k + kk;
+        double* crow = c + row * Q + e;
+        for (int b = bl; b < ra1; b += b_lanes) {
+          double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (j < m) {
+              const double av = staged ? As[(aa * m + j) * ra1 + b]
+                                       : (pc.mode == 1 ? __ldg(a + ((int64_t)aa * pc.n + i) * ra1 + b)
+                                                       : __ldg(a + (((int64_t)aa * pc.n + i) * pc.m + j) * ra1 + b));
+              y0 = fma(av, x0[j], y0);
+              y1 = fma(av, x1[j], y1);
+            }
+          }
+          double* dst = crow + (int64_t)b * rb1;
+          if (aligned && two) {
+            st_cs2(dst, y0, y1);
+          } else {
+            dst[0] = y0;
+            if (two) dst[1] = y1;
+          }
+        }
+      }
     }
   }
 }
@@ -113,17 +148,16 @@ int launch_product(const qtt_layout* LA, const double* a, const qtt_layout* LB, 
       pc.m = (int)LA->cols[l];
       pc.k = LB->is_matrix ? (int)LB->cols[l] : 1;
       if (LB->rows[l] != pc.m) return kInvalid;
+      if (pc.m > 4) return kUnsupported;
     }
     if (LC->ranks[l] != (int64_t)pc.ra0 * pc.rb0 || LC->ranks[l + 1] != (int64_t)pc.ra1 * pc.rb1)
       return kInvalid;
-    if (LC->offsets[l] % 2 != 0) return kInvalid;
     pc.unit_begin = units;
-    const int64_t total = (int64_t)pc.ra0 * pc.rb0 * pc.n * pc.k * pc.ra1 * pc.rb1;
-    units += ceil_div(total, kUnit);
+    units += (int64_t)pc.rb0 * pc.n * pc.k;  // one block per (c, i, kk) slab
   }
   desc.total_units = units;
   if (units == 0) return kOk;
-  const int grid = (int)std::min<int64_t>(units, (int64_t)num_sms() * 16);
+  const int grid = (int)std::min<int64_t>(units, (int64_t)num_sms() * 32);
   core_product_kernel<<<grid, kProdThreads, 0, s>>>(desc, a, b, c);
   QTT_CHECK_LAUNCH();
   return kOk;
@@ -151,7 +185,7 @@ struct StructDesc {
   StructCore c[QTT_MAX_CORES * 2];
 };
 
-__global__ void struct_kernel(StructDesc desc, const double* __restrict__ X,
+__global__ void struct_kernel(const __grid_constant__ StructDesc desc, const double* __restrict__ X,
                               const double* __restrict__ Y, double* __restrict__ O) {
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < desc.total;
        g += (int64_t)gridDim.x * blockDim.x) {
