@@ -293,6 +293,9 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_sample()
+    extras = None
+    if rank == 0 and not args.no_extras:
+        extras = run_extras(torch, T, cpu_baseline=(world == 1 and not args.no_cpu_baseline))
 
     if rank == 0:
         line = {
@@ -344,11 +347,94 @@ def run_ours(args):
             },
             "clocks": clk,
             "cpu_baseline": cpu,
+            "extras": extras,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+SURVEY_C3_TTSVD_RANKS = (1, 2, 4, 5, 6, 6, 6, 6, 6, 7, 7, 9, 10, 10, 11, 13, 14, 16, 17, 19, 23, 23, 16, 8, 4, 2, 1)
+
+
+def _dev_ms(torch, fn):
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return out, e0.elapsed_time(e1)
+
+
+def run_extras(torch, T, cpu_baseline=True) -> dict:
+    """Configs 3, 1 and the 2^10 x 2^10 solve (config-4 geometry/BCs/load with
+    constant E; see DESIGN.md for the variable-E case), device-timed."""
+    import time as _t
+
+    out = {}
+    # ---- config 3: rounding of a 16-term rank-8 sum (d=26) and TT-SVD of 2^26
+    rng = np.random.default_rng(3000)
+    acc = None
+    for _ in range(16):
+        rk = [1] + [8] * 25 + [1]
+        t = T.TTVector([rng.standard_normal((rk[k], 2, rk[k + 1])) / np.sqrt(8) for k in range(26)])
+        acc = t if acc is None else T.tt_add(acc, t)
+    c3 = {}
+    for eps in (1e-6, 1e-10):
+        T.tt_round(acc, eps)
+        r, ms = _dev_ms(torch, lambda: T.tt_round(acc, eps))
+        c3[f"round_eps{eps:g}_ms"] = round(ms, 3)
+        c3[f"round_eps{eps:g}_ranks_unchanged"] = r.ranks == tuple([1] + [min(128, 2**k, 2 ** (26 - k)) for k in range(1, 26)] + [1])
+    n = 1 << 13
+    xs = torch.arange(n, dtype=torch.float64, device="cuda") / (n - 1)
+    X, Y = torch.meshgrid(xs, xs, indexing="ij")
+    from paper_2501_07778_b200.assembly import _flat_ordered
+
+    v = _flat_ordered(torch.sin(3 * X) * torch.exp(-Y) + 0.1 * torch.cos(7 * X * Y), "zorder")
+    T.tt_decompose(v, 1e-8)
+    tv, ms = _dev_ms(torch, lambda: T.tt_decompose(v, 1e-8))
+    c3["ttsvd_2^26_ms"] = round(ms, 3)
+    c3["ttsvd_ranks_equal_reference"] = tv.ranks == SURVEY_C3_TTSVD_RANKS
+    c3["ttsvd_hbm_roofline_ms"] = round(4.17e9 / 6543.4e9 * 1e3, 3)
+    c3["reference_cpu_s"] = {"round_each_eps": 0.175, "ttsvd": 10.59, "source": "SURVEY Appendix B, 8-core Xeon"}
+    out["config3"] = c3
+    # ---- solves
+    from paper_2501_07778_b200 import solver as S
+    from paper_2501_07778_b200.configs import build_system
+
+    solves = {}
+    for idx, d in ((1, 5), (40, 10)):
+        tm = {}
+        torch.cuda.synchronize()
+        t0 = _t.perf_counter()
+        gsys, eps = build_system(idx, d, tm)
+        t1 = _t.perf_counter()
+        res = S.solve(gsys.K, gsys.f, S.SolverConfig(epsilon=eps, seed=0, local_solver="direct"))
+        torch.cuda.synchronize()
+        t2 = _t.perf_counter()
+        solves[f"config{idx if idx != 40 else '4_constE'}_d{d}"] = {
+            "build_s": round(t1 - t0, 3), **{k: round(v, 3) for k, v in tm.items()},
+            "solve_s": round(t2 - t1, 3), "total_s": round(t2 - t0, 3), "sweeps": res.sweeps,
+            "residual": res.residual, "converged": res.converged, "max_rank": max(res.u.ranks),
+            "K_max_rank": max(gsys.K.ranks),
+        }
+    solves["reference_cpu_s"] = {"config1_d5_solve": 1.21, "config4_constE_d10_solve": 658.9,
+                                 "config4_constE_d10_assembly": 11.05, "source": "SURVEY Appendix B, 8-core Xeon"}
+    if cpu_baseline:
+        # reference algorithm (oracle restatement) on this host: config 1 solve
+        from oracle import amen
+
+        gsys, eps = build_system(1, 5)
+        K = [c.cpu().numpy() for c in gsys.K.cores]
+        f = [c.cpu().numpy() for c in gsys.f.cores]
+        t0 = _t.perf_counter()
+        r = amen.solve(K, f, eps=eps, seed=0)
+        solves["cpu_oracle_config1_d5_solve_s"] = round(_t.perf_counter() - t0, 3)
+        solves["cpu_oracle_config1_sweeps"] = r["sweeps"]
+    out["solves"] = solves
+    return out
 
 
 def load_peaks() -> dict:
@@ -458,6 +544,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

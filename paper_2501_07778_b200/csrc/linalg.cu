@@ -654,32 +654,88 @@ int set_identity(cudaStream_t s, int rows, int cols, double* A, int64_t lda) {
   return kOk;
 }
 
+// Side stream for the look-ahead panel factorisation (one per process).
+static cudaStream_t side_stream() {
+  static cudaStream_t st = nullptr;
+  if (!st) {
+    // highest priority: the panel (critical path) is scheduled ahead of the
+    // trailing-update GEMM blocks as soon as SMs free up
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi);
+  }
+  return st;
+}
+
 int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
        double* R, int64_t ldr) {
   if (m <= 0 || n <= 0) return kInvalid;
   const int k = std::min(m, n);
   if (ceil_div(m, PMAXROWS) > PMAXCLUSTER) return kUnsupported;
-  double *Ac, *V, *Y, *Y2, *tau, *W;
+  double *Ac, *V, *Y, *Y2, *tau, *W, *W1;
   const int64_t mm = m;
   QTT_CUDA(cudaMallocAsync(&Ac, sizeof(double) * mm * n, s));
   QTT_CUDA(cudaMallocAsync(&V, sizeof(double) * mm * k, s));
-  QTT_CUDA(cudaMallocAsync(&Y, sizeof(double) * mm * PNB, s));
+  QTT_CUDA(cudaMallocAsync(&Y, sizeof(double) * mm * k, s));
   QTT_CUDA(cudaMallocAsync(&Y2, sizeof(double) * mm * k, s));
   QTT_CUDA(cudaMallocAsync(&tau, sizeof(double) * (k + 1), s));
   QTT_CUDA(cudaMallocAsync(&W, sizeof(double) * PNB * (int64_t)std::max(n, k), s));
+  QTT_CUDA(cudaMallocAsync(&W1, sizeof(double) * PNB * PNB, s));
   QTT_TRY(copy_matrix(s, m, n, A, lda, Ac, m));
+  // Look-ahead: after panel p, update only panel p+1's columns, factor panel
+  // p+1 on a side stream while the rest of the trailing matrix is updated,
+  // so the latency-bound panel overlaps the DMMA update.
+  static cudaEvent_t ev_cols = nullptr, ev_panel = nullptr;
+  if (!ev_cols) {
+    QTT_CUDA(cudaEventCreateWithFlags(&ev_cols, cudaEventDisableTiming));
+    QTT_CUDA(cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming));
+  }
+  cudaStream_t sb = side_stream();
+  auto panel_args = [&](int j0) {
+    const int nb = std::min(PNB, k - j0);
+    return PanelArgs{m - j0, nb, 0, Ac + j0 + (int64_t)j0 * m, mm, V + j0 + (int64_t)j0 * m, mm,
+                     Y + j0 + (int64_t)j0 * m, mm, Y2 + j0 + (int64_t)j0 * m, mm, tau + j0};
+  };
+  static const bool lookahead = getenv("QTT_NO_LOOKAHEAD") == nullptr;
+  if (!lookahead) {
+    for (int j0 = 0; j0 < k; j0 += PNB) {
+      const int nb = std::min(PNB, k - j0);
+      const int mp = m - j0, nt = n - j0 - nb;
+      QTT_TRY(launch_panel(s, panel_args(j0)));
+      if (nt > 0) {
+        double* At = Ac + j0 + (int64_t)(j0 + nb) * m;
+        QTT_TRY(dgemm(s, 1, 0, nb, nt, mp, 1.0, V + j0 + (int64_t)j0 * m, mm, At, mm, 0.0, W, nb));
+        QTT_TRY(dgemm(s, 0, 0, mp, nt, nb, -1.0, Y + j0 + (int64_t)j0 * m, mm, W, nb, 1.0, At, mm));
+      }
+    }
+  } else {
+  QTT_TRY(launch_panel(s, panel_args(0)));
   for (int j0 = 0; j0 < k; j0 += PNB) {
     const int nb = std::min(PNB, k - j0);
     const int mp = m - j0;
-    PanelArgs pa{mp, nb, 0, Ac + j0 + (int64_t)j0 * m, mm, V + j0 + (int64_t)j0 * m, mm,
-                 Y + j0, mm, Y2 + j0 + (int64_t)j0 * m, mm, tau + j0};
-    QTT_TRY(launch_panel(s, pa));
     const int nt = n - j0 - nb;
-    if (nt > 0) {
-      double* At = Ac + j0 + (int64_t)(j0 + nb) * m;
-      QTT_TRY(dgemm(s, 1, 0, nb, nt, mp, 1.0, V + j0 + (int64_t)j0 * m, mm, At, mm, 0.0, W, nb));
-      QTT_TRY(dgemm(s, 0, 0, mp, nt, nb, -1.0, Y + j0, mm, W, nb, 1.0, At, mm));
+    if (nt <= 0) break;
+    const double* Vp = V + j0 + (int64_t)j0 * m;
+    const double* Yp = Y + j0 + (int64_t)j0 * m;
+    const int jn = j0 + nb;
+    const int nb_next = jn < k ? std::min(PNB, k - jn) : 0;
+    if (nb_next > 0) {
+      double* An = Ac + j0 + (int64_t)jn * m;
+      QTT_TRY(dgemm(s, 1, 0, nb, nb_next, mp, 1.0, Vp, mm, An, mm, 0.0, W1, nb));
+      QTT_TRY(dgemm(s, 0, 0, mp, nb_next, nb, -1.0, Yp, mm, W1, nb, 1.0, An, mm));
+      QTT_CUDA(cudaEventRecord(ev_cols, s));
+      QTT_CUDA(cudaStreamWaitEvent(sb, ev_cols, 0));
+      QTT_TRY(launch_panel(sb, panel_args(jn)));
+      QTT_CUDA(cudaEventRecord(ev_panel, sb));
     }
+    const int rest = nt - nb_next;
+    if (rest > 0) {
+      double* Ar = Ac + j0 + (int64_t)(jn + nb_next) * m;
+      QTT_TRY(dgemm(s, 1, 0, nb, rest, mp, 1.0, Vp, mm, Ar, mm, 0.0, W, nb));
+      QTT_TRY(dgemm(s, 0, 0, mp, rest, nb, -1.0, Yp, mm, W, nb, 1.0, Ar, mm));
+    }
+    if (nb_next > 0) QTT_CUDA(cudaStreamWaitEvent(s, ev_panel, 0));
+  }
   }
   if (R) {
     upper_copy_kernel<<<grid_for((int64_t)k * n), 256, 0, s>>>(k, n, Ac, mm, R, ldr);
@@ -702,6 +758,7 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
   QTT_CUDA(cudaFreeAsync(Y2, s));
   QTT_CUDA(cudaFreeAsync(tau, s));
   QTT_CUDA(cudaFreeAsync(W, s));
+  QTT_CUDA(cudaFreeAsync(W1, s));
   return kOk;
 }
 

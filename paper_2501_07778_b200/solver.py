@@ -40,6 +40,24 @@ from .ttcore import (
 __all__ = ["SolverConfig", "SolveOutcome", "solve", "residual", "apply_tt_matrix"]
 
 _DENSE_LOCAL_LIMIT = 1200  # kept for API parity (solver.py:23); local solves are direct
+
+# Optional phase timing (synchronising; diagnostics only): set PROFILE = {}.
+PROFILE = None
+
+
+class _phase:
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        if PROFILE is not None:
+            torch.cuda.synchronize()
+            self.t = time.perf_counter()
+
+    def __exit__(self, *exc):
+        if PROFILE is not None:
+            torch.cuda.synchronize()
+            PROFILE[self.name] = PROFILE.get(self.name, 0.0) + time.perf_counter() - self.t
 _DENSE_RESIDUAL_BITS = 22  # materialise vectors up to 2^22 entries (solver.py:24)
 
 
@@ -176,8 +194,10 @@ def _local_matrix_cm(phi_l, a_p, phi_r):
 def _solve_local(phi_l, a_p, phi_r, rhs):
     rl, n, rr = rhs.shape
     dim = rl * n * rr
-    mcm = _local_matrix_cm(phi_l, a_p, phi_r)
-    sol, _ = dense_solve_colmajor(mcm, dim, rhs.reshape(-1))
+    with _phase("local_matrix"):
+        mcm = _local_matrix_cm(phi_l, a_p, phi_r)
+    with _phase("local_lu"):
+        sol, _ = dense_solve_colmajor(mcm, dim, rhs.reshape(-1))
     return sol.view(rl, n, rr)
 
 
@@ -338,7 +358,8 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig) -> SolveOutcome:
             rhs = _local_rhs(psi_l[k], F[k], psi_r[k + 1])
             xk = _solve_local(phi_l[k], A[k], phi_r[k + 1], rhs)
             if k > 0:
-                x[k], carry = _truncated_split_right(xk, delta, cfg.max_rank)
+                with _phase("svd_split"):
+                    x[k], carry = _truncated_split_right(xk, delta, cfg.max_rank)
                 p0, pn, p1 = x[k - 1].shape
                 x[k - 1] = mm(x[k - 1].reshape(p0 * pn, p1), carry).view(p0, pn, carry.shape[1])
                 phi_r[k] = _phi_right(phi_r[k + 1], x[k], A[k], x[k])
@@ -351,7 +372,8 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig) -> SolveOutcome:
         sweeps_done = sweep + 1
         rank_history.append(max(c.shape[0] for c in x[1:]) if d > 1 else 1)
         u = _concat(TTVector, x)
-        res = residual(K, u, f)
+        with _phase("residual"):
+            res = residual(K, u, f)
         residual_history.append(float(res))
         if res <= cfg.epsilon:
             break

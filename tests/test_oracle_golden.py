@@ -114,3 +114,24 @@ def test_coupling_golden(name):
     for tag, t in (("K", K), ("f", f), ("mask", tau), ("Kd", Kd), ("fd", fd)):
         assert O.ranks(t) == tuple(g[f"{name}_{tag}_ranks"]), tag
         assert rel(O.full(t), g[f"{name}_{tag}"]) < 1e-11, tag
+
+
+@pytest.mark.parametrize("name", ["single3", "lshape2", "cantilever2"])
+def test_oracle_amen_matches_reference_solution(name):
+    from oracle import amen
+
+    g = load("coupling")
+    spec = cases.coupling_cases()[name]
+    meshes = [mesh_of(s) for s in spec["meshes"]]
+    topo = DomainTopology.from_subdomains(meshes)
+    mat = MaterialModel(*spec["material"])
+    systems = F.assemble_all(meshes, mat, "zorder", spec["eps"], spec["body"])
+    K, f, tau, gam = F.concat(systems, topo, None, "zorder", spec["eps"])
+    Kd, fd = F.dirichlet(K, f, tau, gam, None, spec["eps"])
+    out = amen.solve(Kd, fd, eps=spec["solve"], seed=0)
+    assert out["converged"]
+    kd, fdd = g[f"{name}_Kd"], g[f"{name}_fd"]
+    u_exact = np.linalg.solve(kd, fdd)
+    err = rel(O.full(out["u"]), u_exact)
+    ref_err = rel(g[f"{name}_u"], u_exact)
+    assert err <= max(10 * ref_err, np.linalg.cond(kd) * spec["solve"]) + 1e-10

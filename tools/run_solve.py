@@ -7,6 +7,8 @@ ap = argparse.ArgumentParser(); ap.add_argument('--config', type=int, default=1)
 ap.add_argument('--max-sweeps', type=int, default=40); ap.add_argument('--no-solve', action='store_true'); ap.add_argument('--dense-bits', type=int, default=22)
 a = ap.parse_args()
 S._DENSE_RESIDUAL_BITS = a.dense_bits
+import os
+if os.environ.get('QTT_SOLVER_PROFILE'): S.PROFILE = {}
 tm = {}
 t0 = time.perf_counter()
 gsys, eps = build_system(a.config, a.d, tm)
@@ -19,4 +21,4 @@ torch.cuda.synchronize()
 t2 = time.perf_counter()
 print(json.dumps({'config': a.config, 'd': a.d, 'solve_s': t2 - t1, 'total_s': t2 - t0, 'sweeps': out.sweeps,
                   'residual': out.residual, 'converged': out.converged, 'u_ranks': out.u.ranks,
-                  'res_hist': out.residual_history, 'rank_hist': out.rank_history}), flush=True)
+                  'res_hist': out.residual_history, 'rank_hist': out.rank_history, 'profile': S.PROFILE}), flush=True)
