@@ -74,6 +74,7 @@ const char* qtt_version(void) { return "qtt_b200 0.1 sm_100a fp64"; }
 long long qtt_launch_count(void) { return g_launches.load(); }
 
 int qtt_profile_gemm(int32_t on) {
+  pool_init();
   GemmProfile& p = gemm_profile();
   for (auto& e : p.events) {
     cudaEventDestroy(e.first);
@@ -87,6 +88,7 @@ int qtt_profile_gemm(int32_t on) {
 }
 
 int qtt_profile_gemm_read(double* flops, double* ms, int64_t* launches) {
+  pool_init();
   GemmProfile& p = gemm_profile();
   double tot = 0.0;
   for (auto& e : p.events) {
@@ -105,96 +107,113 @@ int64_t qtt_layout_size(const qtt_layout* lay) { return valid(lay) ? packed_size
 
 int qtt_matvec(const qtt_layout* A, const double* a, const qtt_layout* x, const double* xd,
                const qtt_layout* y, double* yd, void* stream) {
+  pool_init();
   if (!valid(A) || !valid(x) || !valid(y) || !A->is_matrix || x->is_matrix) return QTT_EINVAL;
   return product(A, a, x, xd, y, yd, 0, S(stream));
 }
 
 int qtt_matmat(const qtt_layout* A, const double* a, const qtt_layout* B, const double* b,
                const qtt_layout* C, double* c, void* stream) {
+  pool_init();
   if (!valid(A) || !valid(B) || !valid(C) || !A->is_matrix || !B->is_matrix) return QTT_EINVAL;
   return product(A, a, B, b, C, c, 0, S(stream));
 }
 
 int qtt_hadamard(const qtt_layout* A, const double* a, const qtt_layout* B, const double* b,
                  const qtt_layout* C, double* c, void* stream) {
+  pool_init();
   if (!valid(A) || !valid(B) || !valid(C)) return QTT_EINVAL;
   return product(A, a, B, b, C, c, 1, S(stream));
 }
 
 int qtt_add(const qtt_layout* A, const double* a, const qtt_layout* B, const double* b,
             double beta, const qtt_layout* C, double* c, void* stream) {
+  pool_init();
   if (!valid(A) || !valid(B) || !valid(C)) return QTT_EINVAL;
   return add(A, a, B, b, beta, C, c, S(stream));
 }
 
 int qtt_zkron(const qtt_layout* A, const double* a, const qtt_layout* B, const double* b,
               const qtt_layout* C, double* c, void* stream) {
+  pool_init();
   if (!valid(A) || !valid(B) || !valid(C)) return QTT_EINVAL;
   return zkron(A, a, B, b, C, c, S(stream));
 }
 
 int qtt_diag(const qtt_layout* V, const double* v, const qtt_layout* D, double* dd, void* stream) {
+  pool_init();
   if (!valid(V) || !valid(D)) return QTT_EINVAL;
   return diag(V, v, D, dd, S(stream));
 }
 
 int qtt_transpose(const qtt_layout* A, const double* a, const qtt_layout* T, double* t,
                   void* stream) {
+  pool_init();
   if (!valid(A) || !valid(T)) return QTT_EINVAL;
   return transpose_tt(A, a, T, t, S(stream));
 }
 
 int qtt_scale(const qtt_layout* A, const double* a, double s, double* out, void* stream) {
+  pool_init();
   if (!valid(A)) return QTT_EINVAL;
   return scale_copy(A, a, s, out, S(stream));
 }
 
 int qtt_round(const qtt_layout* in, const double* in_data, double eps, qtt_layout* out,
               double* out_data, void* stream) {
+  pool_init();
   if (!valid(in) || !out || eps < 0) return QTT_EINVAL;
   return round_tt(in, in_data, eps, out, out_data, S(stream));
 }
 
 int qtt_decompose(const double* dense, int32_t d, const int64_t* sizes, double eps,
                   qtt_layout* out, double* out_data, int64_t out_capacity, void* stream) {
+  pool_init();
   if (!dense || !sizes || !out || eps < 0) return QTT_EINVAL;
   return decompose(dense, d, sizes, eps, out, out_data, out_capacity, S(stream));
 }
 
 int qtt_norm(const qtt_layout* A, const double* a, double* result, void* stream) {
+  pool_init();
   if (!valid(A) || !result) return QTT_EINVAL;
   return norm_orth(A, a, result, S(stream));
 }
 
 int qtt_dot(const qtt_layout* A, const double* a, const qtt_layout* B, const double* b,
             double* result, void* stream) {
+  pool_init();
   if (!valid(A) || !valid(B) || !result) return QTT_EINVAL;
   return dot(A, a, B, b, result, S(stream));
 }
 
 int qtt_contract(const qtt_layout* A, const double* a, double* dense, void* stream) {
+  pool_init();
   if (!valid(A)) return QTT_EINVAL;
   return contract(A, a, dense, S(stream));
 }
 
 int qtt_dense_apply(const qtt_layout* A, const double* a, const double* v, double* out,
                     void* stream) {
+  pool_init();
   if (!valid(A) || !A->is_matrix) return QTT_EINVAL;
   return dense_apply(A, a, v, out, S(stream));
 }
 
 int qtt_zorder_permutation(int32_t d, int64_t* perm, void* stream) {
+  pool_init();
   if (d < 1 || d > 30) return QTT_EINVAL;
   return zorder_perm(d, perm, 0, S(stream));
 }
 
 int qtt_zorder_dof_permutation(int32_t d, int64_t* perm, void* stream) {
+  pool_init();
   if (d < 1 || d > 30) return QTT_EINVAL;
   return zorder_perm(d, perm, 1, S(stream));
 }
 
 int qtt_z_index(int32_t d, int64_t count, const int64_t* i, const int64_t* j, int64_t* z,
                 void* stream) {
+  pool_init();
   if (d < 1 || d > 31 || count < 0) return QTT_EINVAL;
   return z_index(d, count, i, j, z, S(stream));
 }
@@ -202,6 +221,7 @@ int qtt_z_index(int32_t d, int64_t count, const int64_t* i, const int64_t* j, in
 int qtt_gemm(int32_t trans_a, int32_t trans_b, int64_t m, int64_t n, int64_t k, double alpha,
              const double* a, int64_t lda, const double* b, int64_t ldb, double beta, double* c,
              int64_t ldc, void* stream) {
+  pool_init();
   if (m < 0 || n < 0 || k < 0 || m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff)
     return QTT_EINVAL;
   return dgemm(S(stream), trans_a, trans_b, (int)m, (int)n, (int)k, alpha, a, lda, b, ldb, beta, c,
@@ -210,12 +230,14 @@ int qtt_gemm(int32_t trans_a, int32_t trans_b, int64_t m, int64_t n, int64_t k, 
 
 int qtt_qr(int64_t m, int64_t n, const double* a, int64_t lda, double* q, int64_t ldq, double* r,
            int64_t ldr, void* stream) {
+  pool_init();
   if (m < 1 || n < 1 || m > 0x7fffffff || n > 0x7fffffff) return QTT_EINVAL;
   return qr(S(stream), (int)m, (int)n, a, lda, q, ldq, r, ldr);
 }
 
 int qtt_svd(int64_t m, int64_t n, const double* a, int64_t lda, double* s, double* u, int64_t ldu,
             void* stream) {
+  pool_init();
   if (m < 1 || n < 1 || m > 0x7fffffff || n > 0x7fffffff) return QTT_EINVAL;
   cudaStream_t st = S(stream);
   const int M = (int)m, N = (int)n, k = std::min(M, N);

@@ -87,6 +87,12 @@ struct GemmArgs {
 
 int gemm(const GemmArgs& g, cudaStream_t stream);
 
+// Keep freed stream-ordered allocations cached in the device's default pool
+// (release threshold = max): the TT sweeps allocate and free workspaces on
+// every step, and trimming the pool at each synchronisation would re-map
+// memory every time.  Called by every C-ABI entry point.
+void pool_init();
+
 // Optional per-launch GEMM timing (CUDA events on the launching stream) used
 // by bench.py to report the DMMA kernel's achieved FLOP rate.
 struct GemmProfile {

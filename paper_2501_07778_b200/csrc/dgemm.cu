@@ -207,6 +207,18 @@ __global__ void copy_matrix_kernel(int rows, int cols, const double* __restrict_
 
 }  // namespace
 
+void pool_init() {
+  static bool done[64] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 GemmProfile& gemm_profile() {
   static GemmProfile p;
   return p;

@@ -113,6 +113,7 @@ extern "C" int qtt_element_grids(int32_t d, int32_t zorder, int32_t ngauss, cons
   if (d < 1 || d > 15 || ngauss < 1 || ngauss > 4 || !coef || !cmat || !degenerate)
     return QTT_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  pool_init();
   ElemCoef ec;
   ec.ng = ngauss;
   ec.d = d;

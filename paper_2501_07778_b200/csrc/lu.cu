@@ -222,6 +222,7 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
 extern "C" int qtt_dense_solve(int64_t n, const double* m, int64_t ldm, const double* b, double* x,
                                int32_t* fallback, void* stream) {
   if (n < 1 || n > 0x7fffffff || !fallback) return QTT_EINVAL;
+  qtt::pool_init();
   int fb = 0;
   int st = qtt::dense_solve(reinterpret_cast<cudaStream_t>(stream), (int)n, m, ldm, b, x, &fb);
   *fallback = fb;
