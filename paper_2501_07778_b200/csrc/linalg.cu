@@ -16,7 +16,7 @@ namespace {
 constexpr double kEps = 2.220446049250313e-16;
 
 // ------------------------------------------------------------------ panel QR
-constexpr int PNB = 32;          // panel width
+
 constexpr int PTHREADS = 512;    // 16 warps per CTA
 constexpr int PMAXROWS = 736;    // panel rows held per CTA (736*32*8 B = 184 KB)
 constexpr int PMAXCLUSTER = 16;  // non-portable cluster size (B200: 16 SMs per cluster)
@@ -49,6 +49,7 @@ __device__ __forceinline__ void panel_barrier(cg::cluster_group& cl, int cs) {
   else cl.sync();
 }
 
+template <int PNB>
 __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
   extern __shared__ double smem[];
   cg::cluster_group cluster = cg::this_cluster();
@@ -168,31 +169,34 @@ __global__ void __launch_bounds__(PTHREADS) panel_qr_kernel(PanelArgs pa) {
   if (crank == 0 && tid < nb) pa.tau[tid] = tau_s[tid];
 }
 
-size_t panel_smem_bytes(int rpc) {
+constexpr int PMAXROWS16 = 1600;  // rows per CTA for the 16-wide panels of very tall matrices
+
+size_t panel_smem_bytes(int rpc, int pnb) {
   return sizeof(double) *
-         ((size_t)rpc * PNB + 2 * PMAXCLUSTER * 2 * PNB + 2 * PNB + PNB * PNB + PNB);
+         ((size_t)rpc * pnb + 2 * PMAXCLUSTER * 2 * pnb + 2 * pnb + pnb * pnb + pnb);
 }
 
-int launch_panel(cudaStream_t s, const PanelArgs& pa0) {
+template <int PNB>
+int launch_panel_t(cudaStream_t s, const PanelArgs& pa0, int maxrows) {
   static bool configured = false;
   if (!configured) {
-    QTT_CUDA(cudaFuncSetAttribute(panel_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)panel_smem_bytes(PMAXROWS)));
-    QTT_CUDA(cudaFuncSetAttribute(panel_qr_kernel,
+    QTT_CUDA(cudaFuncSetAttribute(panel_qr_kernel<PNB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)panel_smem_bytes(maxrows, PNB)));
+    QTT_CUDA(cudaFuncSetAttribute(panel_qr_kernel<PNB>,
                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     configured = true;
   }
   PanelArgs pa = pa0;
   // spread tall panels over up to 16 CTAs (>= 256 rows each) so the
   // per-column work per CTA stays small; single CTA below 384 rows.
-  int cs = (int)std::max<int64_t>(ceil_div(pa.m, PMAXROWS), std::min<int64_t>(16, pa.m / 256));
+  int cs = (int)std::max<int64_t>(ceil_div(pa.m, maxrows), std::min<int64_t>(16, pa.m / 256));
   cs = std::max(cs, 1);
   if (cs > PMAXCLUSTER) return kUnsupported;
   pa.rpc = (int)ceil_div(pa.m, cs);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs, 1, 1);
   cfg.blockDim = dim3(PTHREADS, 1, 1);
-  cfg.dynamicSmemBytes = panel_smem_bytes(pa.rpc);
+  cfg.dynamicSmemBytes = panel_smem_bytes(pa.rpc, PNB);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -201,9 +205,17 @@ int launch_panel(cudaStream_t s, const PanelArgs& pa0) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  QTT_CUDA(cudaLaunchKernelEx(&cfg, panel_qr_kernel, pa));
+  QTT_CUDA(cudaLaunchKernelEx(&cfg, panel_qr_kernel<PNB>, pa));
   note_launch();
   return kOk;
+}
+
+// Panel width: 32 columns while a 16-CTA cluster holds the rows, else 16.
+inline int panel_width(int m) { return m <= PMAXCLUSTER * PMAXROWS ? 32 : 16; }
+
+int launch_panel(cudaStream_t s, const PanelArgs& pa) {
+  return pa.nb > 16 || panel_width(pa.m + 0) == 32 ? launch_panel_t<32>(s, pa, PMAXROWS)
+                                                   : launch_panel_t<16>(s, pa, PMAXROWS16);
 }
 
 __global__ void upper_copy_kernel(int k, int n, const double* __restrict__ A, int64_t lda,
@@ -671,7 +683,8 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
        double* R, int64_t ldr) {
   if (m <= 0 || n <= 0) return kInvalid;
   const int k = std::min(m, n);
-  if (ceil_div(m, PMAXROWS) > PMAXCLUSTER) return kUnsupported;
+  if (ceil_div(m, PMAXROWS16) > PMAXCLUSTER) return kUnsupported;
+  const int PW = panel_width(m);
   double *Ac, *V, *Y, *Y2, *tau, *W, *W1;
   const int64_t mm = m;
   QTT_CUDA(cudaMallocAsync(&Ac, sizeof(double) * mm * n, s));
@@ -679,8 +692,8 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
   QTT_CUDA(cudaMallocAsync(&Y, sizeof(double) * mm * k, s));
   QTT_CUDA(cudaMallocAsync(&Y2, sizeof(double) * mm * k, s));
   QTT_CUDA(cudaMallocAsync(&tau, sizeof(double) * (k + 1), s));
-  QTT_CUDA(cudaMallocAsync(&W, sizeof(double) * PNB * (int64_t)std::max(n, k), s));
-  QTT_CUDA(cudaMallocAsync(&W1, sizeof(double) * PNB * PNB, s));
+  QTT_CUDA(cudaMallocAsync(&W, sizeof(double) * PW * (int64_t)std::max(n, k), s));
+  QTT_CUDA(cudaMallocAsync(&W1, sizeof(double) * PW * PW, s));
   QTT_TRY(copy_matrix(s, m, n, A, lda, Ac, m));
   // Look-ahead: after panel p, update only panel p+1's columns, factor panel
   // p+1 on a side stream while the rest of the trailing matrix is updated,
@@ -692,14 +705,14 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
   }
   cudaStream_t sb = side_stream();
   auto panel_args = [&](int j0) {
-    const int nb = std::min(PNB, k - j0);
+    const int nb = std::min(PW, k - j0);
     return PanelArgs{m - j0, nb, 0, Ac + j0 + (int64_t)j0 * m, mm, V + j0 + (int64_t)j0 * m, mm,
                      Y + j0 + (int64_t)j0 * m, mm, Y2 + j0 + (int64_t)j0 * m, mm, tau + j0};
   };
   static const bool lookahead = getenv("QTT_NO_LOOKAHEAD") == nullptr;
   if (!lookahead) {
-    for (int j0 = 0; j0 < k; j0 += PNB) {
-      const int nb = std::min(PNB, k - j0);
+    for (int j0 = 0; j0 < k; j0 += PW) {
+      const int nb = std::min(PW, k - j0);
       const int mp = m - j0, nt = n - j0 - nb;
       QTT_TRY(launch_panel(s, panel_args(j0)));
       if (nt > 0) {
@@ -710,15 +723,15 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
     }
   } else {
   QTT_TRY(launch_panel(s, panel_args(0)));
-  for (int j0 = 0; j0 < k; j0 += PNB) {
-    const int nb = std::min(PNB, k - j0);
+  for (int j0 = 0; j0 < k; j0 += PW) {
+    const int nb = std::min(PW, k - j0);
     const int mp = m - j0;
     const int nt = n - j0 - nb;
     if (nt <= 0) break;
     const double* Vp = V + j0 + (int64_t)j0 * m;
     const double* Yp = Y + j0 + (int64_t)j0 * m;
     const int jn = j0 + nb;
-    const int nb_next = jn < k ? std::min(PNB, k - jn) : 0;
+    const int nb_next = jn < k ? std::min(PW, k - jn) : 0;
     if (nb_next > 0) {
       double* An = Ac + j0 + (int64_t)jn * m;
       QTT_TRY(dgemm(s, 1, 0, nb, nb_next, mp, 1.0, Vp, mm, An, mm, 0.0, W1, nb));
@@ -743,9 +756,9 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
   }
   if (Q) {
     QTT_TRY(set_identity(s, m, k, Q, ldq));
-    const int last = ((k - 1) / PNB) * PNB;
-    for (int j0 = last; j0 >= 0; j0 -= PNB) {
-      const int nb = std::min(PNB, k - j0);
+    const int last = ((k - 1) / PW) * PW;
+    for (int j0 = last; j0 >= 0; j0 -= PW) {
+      const int nb = std::min(PW, k - j0);
       const int mp = m - j0, kc = k - j0;
       double* Qs = Q + j0 + (int64_t)j0 * ldq;
       QTT_TRY(dgemm(s, 1, 0, nb, kc, mp, 1.0, V + j0 + (int64_t)j0 * m, mm, Qs, ldq, 0.0, W, nb));

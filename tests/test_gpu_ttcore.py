@@ -228,3 +228,22 @@ def test_svd_cluster_path(m, n):
     assert np.abs(s - np.linalg.svd(a, compute_uv=False)).max() <= 1e-14 * 20
     u = U.cpu().numpy().reshape(k, m).T
     assert np.abs(u.T @ u - np.eye(k)).max() < 1e-12
+
+
+def test_qr_very_tall_uses_16_wide_panels():
+    """m > 16*736 rows switches to 16-column panels (config-5 sized QRs)."""
+    from paper_2501_07778_b200 import _lib
+    import ctypes
+
+    m, n = 12500, 40
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((m, n))
+    A = torch.tensor(a.ravel(order="F"), device="cuda")
+    Q = torch.zeros(m * n, dtype=torch.float64, device="cuda")
+    R = torch.zeros(n * n, dtype=torch.float64, device="cuda")
+    _lib.call("qtt_qr", ctypes.c_int64(m), ctypes.c_int64(n), _lib.ptr(A), ctypes.c_int64(m),
+              _lib.ptr(Q), ctypes.c_int64(m), _lib.ptr(R), ctypes.c_int64(n), _lib.stream_handle())
+    q = Q.cpu().numpy().reshape(n, m).T
+    r = R.cpu().numpy().reshape(n, n).T
+    assert np.abs(q @ r - a).max() < 1e-11
+    assert np.abs(q.T @ q - np.eye(n)).max() < 1e-12
