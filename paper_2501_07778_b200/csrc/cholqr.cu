@@ -1,0 +1,190 @@
+// CholeskyQR2 for the large, well-conditioned unfoldings of TT rounding.
+//
+// Householder QR of an m x n matrix needs n sequential column reductions
+// (the panel); for the 4096 x 2048 unfoldings of the BASELINE config-2
+// rounding that latency dominates.  CholeskyQR2 replaces it with four large
+// DMMA GEMMs (A^T A, A R1^{-1}, Q1^T Q1, Q1 R2^{-1}), two blocked Cholesky
+// factorisations of the n x n Gram matrices and two triangular inversions.
+// It is exact-arithmetic QR and numerically orthogonal to O(eps) whenever
+// cond(A) is below ~eps^{-1/2}; the second pass is certified by checking
+// ||Q1^T Q1 - I||_F <= 1/4 (then cond(Q1) <= 1.3 and Q = Q1 R2^{-1} is
+// orthogonal to working accuracy).  Otherwise the caller falls back to
+// Householder (rank-deficient assembly/solver unfoldings).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "linalg.cuh"
+
+namespace qtt {
+namespace {
+
+constexpr int CB = 64;  // Cholesky block
+constexpr int kCholSmem = 2 * CB * (CB + 1) * sizeof(double);
+constexpr int kDefectParts = 296;
+
+// Upper Cholesky of the kb x kb diagonal block (in place, lower part zeroed)
+// and the inverse of the factor into rinv (CB x CB, zero padded).
+__global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* __restrict__ G,
+                                                         int64_t ldg, double* __restrict__ rinv,
+                                                         int* __restrict__ bad) {
+  extern __shared__ double ch_sm[];
+  double (*S)[CB + 1] = reinterpret_cast<double (*)[CB + 1]>(ch_sm);
+  double (*X)[CB + 1] = reinterpret_cast<double (*)[CB + 1]>(ch_sm + CB * (CB + 1));
+  const int tid = threadIdx.x;
+  for (int idx = tid; idx < CB * CB; idx += blockDim.x) {
+    const int r = idx % CB, c = idx / CB;
+    S[r][c] = (r < kb && c < kb) ? G[r + (int64_t)c * ldg] : (r == c ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  for (int j = 0; j < kb; ++j) {
+    const double piv = S[j][j];
+    if (!(piv > 0.0) || !isfinite(piv)) {
+      if (tid == 0) atomicExch(bad, 1);
+      return;  // uniform: every thread reads the same pivot
+    }
+    const double d = sqrt(piv);
+    __syncthreads();
+    for (int c = j + tid; c < kb; c += blockDim.x) S[j][c] = (c == j) ? d : S[j][c] / d;
+    __syncthreads();
+    const int rem = kb - j - 1;
+    for (int idx = tid; idx < rem * rem; idx += blockDim.x) {
+      const int r = j + 1 + idx % rem, c = j + 1 + idx / rem;
+      if (r <= c) S[r][c] = fma(-S[j][r], S[j][c], S[r][c]);
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
+    const int r = idx % kb, c = idx / kb;
+    G[r + (int64_t)c * ldg] = (r <= c) ? S[r][c] : 0.0;
+  }
+  __syncthreads();
+  upper_inverse_smem<CB>(S, X, tid);
+  __syncthreads();
+  for (int idx = tid; idx < CB * CB; idx += blockDim.x) rinv[idx] = X[idx % CB][idx / CB];
+}
+
+// partial sums of squares of (G - I) for the orthogonality certificate
+__global__ void gram_defect_kernel(int n, const double* __restrict__ G, int64_t ldg,
+                                   double* out) {
+  __shared__ double red[32];
+  double a = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)n * n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i % n), c = (int)(i / n);
+    const double v = G[r + (int64_t)c * ldg] - (r == c ? 1.0 : 0.0);
+    a = fma(v, v, a);
+  }
+  a = warp_sum(a);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    out[blockIdx.x] = t;
+  }
+}
+
+__global__ void sum_parts_kernel(int n, const double* __restrict__ part, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += part[i];
+    *out = t;
+  }
+}
+
+// Blocked right-looking upper Cholesky G = R^T R (in place).
+int chol_upper(cudaStream_t s, int n, double* G, int64_t ldg, double* rinv, double* tmp,
+               int* bad) {
+  static bool configured = false;
+  if (!configured) {
+    QTT_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kCholSmem));
+    configured = true;
+  }
+  for (int k0 = 0; k0 < n; k0 += CB) {
+    const int kb = std::min(CB, n - k0);
+    double* Gkk = G + k0 + (int64_t)k0 * ldg;
+    potrf_diag_kernel<<<1, 256, kCholSmem, s>>>(kb, Gkk, ldg, rinv, bad);
+    QTT_CHECK_LAUNCH();
+    const int rest = n - k0 - kb;
+    if (rest <= 0) break;
+    // R12 = R11^{-T} G12  (kb x rest), written back into G12
+    double* G12 = G + k0 + (int64_t)(k0 + kb) * ldg;
+    QTT_TRY(dgemm(s, 1, 0, kb, rest, kb, 1.0, rinv, CB, G12, ldg, 0.0, tmp, kb));
+    QTT_TRY(copy_matrix(s, kb, rest, tmp, kb, G12, ldg));
+    // G22 -= R12^T R12 (full square update; only the upper part is used)
+    double* G22 = G + (k0 + kb) + (int64_t)(k0 + kb) * ldg;
+    QTT_TRY(dgemm(s, 1, 0, rest, rest, kb, -1.0, G12, ldg, G12, ldg, 1.0, G22, ldg));
+    // zero the strictly lower block column below the diagonal block
+    QTT_CUDA(cudaMemset2DAsync(G + (k0 + kb) + (int64_t)k0 * ldg, sizeof(double) * ldg, 0,
+                               sizeof(double) * rest, kb, s));
+  }
+  return kOk;
+}
+
+}  // namespace
+
+int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
+            double* R, int64_t ldr, int* ok) {
+  *ok = 0;
+  if (m < n || n <= 0) return kOk;
+  const int64_t nn = n;
+  double *G, *R1, *Ri, *Q1, *rinv, *tmp, *scal, *parts;
+  int* bad;
+  QTT_CUDA(cudaMallocAsync(&G, sizeof(double) * nn * nn, s));
+  QTT_CUDA(cudaMallocAsync(&R1, sizeof(double) * nn * nn, s));
+  QTT_CUDA(cudaMallocAsync(&Ri, sizeof(double) * nn * nn, s));
+  QTT_CUDA(cudaMallocAsync(&Q1, sizeof(double) * (int64_t)m * nn, s));
+  QTT_CUDA(cudaMallocAsync(&rinv, sizeof(double) * CB * CB, s));
+  QTT_CUDA(cudaMallocAsync(&tmp, sizeof(double) * CB * nn, s));
+  QTT_CUDA(cudaMallocAsync(&scal, sizeof(double) * 4, s));
+  QTT_CUDA(cudaMallocAsync(&parts, sizeof(double) * kDefectParts, s));
+  QTT_CUDA(cudaMallocAsync(&bad, sizeof(int), s));
+  QTT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  int status = kOk;
+  do {
+    // pass 1: G = A^T A = R1^T R1, Q1 = A R1^{-1}
+    if ((status = dgemm(s, 1, 0, n, n, m, 1.0, A, lda, A, lda, 0.0, G, nn)) != kOk) break;
+    if ((status = chol_upper(s, n, G, nn, rinv, tmp, bad)) != kOk) break;
+    int hbad = 0;
+    QTT_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    QTT_CUDA(cudaStreamSynchronize(s));
+    if (hbad) break;
+    QTT_CUDA(cudaMemcpyAsync(R1, G, sizeof(double) * nn * nn, cudaMemcpyDeviceToDevice, s));
+    if ((status = tri_inverse(s, n, R1, nn, Ri)) != kOk) break;
+    if ((status = dgemm(s, 0, 0, m, n, n, 1.0, A, lda, Ri, nn, 0.0, Q1, m)) != kOk) break;
+    // pass 2: certify cond(Q1) ~ 1, then G = Q1^T Q1 = R2^T R2, Q = Q1 R2^{-1}
+    if ((status = dgemm(s, 1, 0, n, n, m, 1.0, Q1, m, Q1, m, 0.0, G, nn)) != kOk) break;
+    gram_defect_kernel<<<kDefectParts, 256, 0, s>>>(n, G, nn, parts);
+    QTT_CHECK_LAUNCH();
+    sum_parts_kernel<<<1, 32, 0, s>>>(kDefectParts, parts, scal);
+    QTT_CHECK_LAUNCH();
+    double defect = 0.0;
+    QTT_CUDA(cudaMemcpyAsync(&defect, scal, sizeof(double), cudaMemcpyDeviceToHost, s));
+    QTT_CUDA(cudaStreamSynchronize(s));
+    if (getenv("QTT_QR_DEBUG")) fprintf(stderr, "[cholqr2] m=%d n=%d defect=%.3e\n", m, n, std::sqrt(defect));
+    if (!(std::sqrt(defect) <= 0.25)) break;
+    if ((status = chol_upper(s, n, G, nn, rinv, tmp, bad)) != kOk) break;
+    QTT_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    QTT_CUDA(cudaStreamSynchronize(s));
+    if (hbad) break;
+    if ((status = tri_inverse(s, n, G, nn, Ri)) != kOk) break;
+    if ((status = dgemm(s, 0, 0, m, n, n, 1.0, Q1, m, Ri, nn, 0.0, Q, ldq)) != kOk) break;
+    // R = R2 R1 (product of upper-triangular factors stays upper triangular)
+    if ((status = dgemm(s, 0, 0, n, n, n, 1.0, G, nn, R1, nn, 0.0, R, ldr)) != kOk) break;
+    *ok = 1;
+  } while (false);
+  QTT_CUDA(cudaFreeAsync(G, s));
+  QTT_CUDA(cudaFreeAsync(R1, s));
+  QTT_CUDA(cudaFreeAsync(Ri, s));
+  QTT_CUDA(cudaFreeAsync(Q1, s));
+  QTT_CUDA(cudaFreeAsync(rinv, s));
+  QTT_CUDA(cudaFreeAsync(tmp, s));
+  QTT_CUDA(cudaFreeAsync(scal, s));
+  QTT_CUDA(cudaFreeAsync(parts, s));
+  QTT_CUDA(cudaFreeAsync(bad, s));
+  return status;
+}
+
+}  // namespace qtt

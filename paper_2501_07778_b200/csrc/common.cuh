@@ -53,6 +53,46 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// X = S^{-1} for an upper-triangular B x B block in shared memory (B = 64,
+// 256 threads): rows bottom-up, all columns of a row in one step, 4 lanes per
+// column splitting the dot product.  Replaces column-per-thread substitution
+// (B^2/2 dependent shared-memory FMAs per thread).
+template <int B>
+__device__ __forceinline__ void upper_inverse_smem(double (*S)[B + 1], double (*X)[B + 1], int tid) {
+  static_assert(B * 4 == 256, "256 threads per block");
+  const int c = tid >> 2, part = tid & 3;
+  for (int r = part; r < B; r += 4) X[r][c] = 0.0;
+  __syncthreads();
+  for (int i = B - 1; i >= 0; --i) {
+    double acc = 0.0;
+    if (c > i)
+      for (int l = i + 1 + part; l <= c; l += 4) acc = fma(S[i][l], X[l][c], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (part == 0 && c >= i) X[i][c] = (c == i) ? 1.0 / S[i][i] : -acc / S[i][i];
+    __syncthreads();
+  }
+}
+
+// X = L^{-1} for the unit lower-triangular part of S (diagonal taken as 1).
+template <int B>
+__device__ __forceinline__ void unit_lower_inverse_smem(double (*S)[B + 1], double (*X)[B + 1],
+                                                        int tid) {
+  static_assert(B * 4 == 256, "256 threads per block");
+  const int c = tid >> 2, part = tid & 3;
+  for (int r = part; r < B; r += 4) X[r][c] = 0.0;
+  __syncthreads();
+  for (int i = 0; i < B; ++i) {
+    double acc = 0.0;
+    if (c < i)
+      for (int l = c + part; l < i; l += 4) acc = fma(S[i][l], X[l][c], acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (part == 0 && c <= i) X[i][c] = (c == i) ? 1.0 : -acc;
+    __syncthreads();
+  }
+}
+
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) {
   return (a + b - 1) / b;
 }

@@ -581,20 +581,11 @@ __global__ void trinv_diag_kernel(int k, const double* __restrict__ R, int64_t l
   const int nb = min(TRB, k - b0);
   for (int idx = threadIdx.x; idx < TRB * TRB; idx += blockDim.x) {
     const int r = idx % TRB, c = idx / TRB;
-    Rs[r][c] = (r < nb && c < nb) ? R[(b0 + r) + (int64_t)(b0 + c) * ldr] : 0.0;
+    Rs[r][c] = (r < nb && c < nb) ? R[(b0 + r) + (int64_t)(b0 + c) * ldr] : (r == c ? 1.0 : 0.0);
     Xs[r][c] = 0.0;
   }
   __syncthreads();
-  const int c = threadIdx.x;
-  if (c < nb) {
-    Xs[c][c] = 1.0 / Rs[c][c];
-    for (int i = c - 1; i >= 0; --i) {
-      double acc = 0.0;
-      for (int l = i + 1; l <= c; ++l) acc = fma(Rs[i][l], Xs[l][c], acc);
-      Xs[i][c] = -acc / Rs[i][i];
-    }
-  }
-  __syncthreads();
+  upper_inverse_smem<TRB>(Rs, Xs, threadIdx.x);
   for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
     const int r = idx % nb, cc = idx / nb;
     X[(b0 + r) + (int64_t)(b0 + cc) * ldx] = Xs[r][cc];
@@ -683,6 +674,22 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
        double* R, int64_t ldr) {
   if (m <= 0 || n <= 0) return kInvalid;
   const int k = std::min(m, n);
+  // Large tall factors: try the GEMM-bound CholeskyQR2 first (certified, falls
+  // back to Householder for ill-conditioned / rank-deficient inputs).
+  static const bool use_chol = getenv("QTT_NO_CHOLQR") == nullptr;
+  if (use_chol && m >= n && n >= 128) {
+    double* Qt = Q;
+    if (!Q) QTT_CUDA(cudaMallocAsync(&Qt, sizeof(double) * (int64_t)m * n, s));
+    double* Rt = R;
+    if (!R) QTT_CUDA(cudaMallocAsync(&Rt, sizeof(double) * (int64_t)n * n, s));
+    int ok = 0;
+    QTT_TRY(cholqr2(s, m, n, A, lda, Qt, Q ? ldq : m, Rt, R ? ldr : n, &ok));
+    if (!Q) QTT_CUDA(cudaFreeAsync(Qt, s));
+    if (!R) QTT_CUDA(cudaFreeAsync(Rt, s));
+    static const bool dbg = getenv("QTT_QR_DEBUG") != nullptr;
+    if (dbg) fprintf(stderr, "[qr] cholqr2 m=%d n=%d %s\n", m, n, ok ? "ok" : "fallback");
+    if (ok) return kOk;
+  }
   if (ceil_div(m, PMAXROWS16) > PMAXCLUSTER) return kUnsupported;
   const int PW = panel_width(m);
   double *Ac, *V, *Y, *Y2, *tau, *W, *W1;
@@ -892,13 +899,10 @@ int frob_norm(cudaStream_t s, int64_t n, const double* x, double* out_dev) {
   return kOk;
 }
 
-int no_truncation_certificate(cudaStream_t s, int k, const double* R, int64_t ldr,
-                              const double* delta_dev, double delta_scale, int* ok_dev) {
-  double *X, *T, *norms;
+int tri_inverse(cudaStream_t s, int k, const double* R, int64_t ldr, double* X) {
+  double* T;
   const int64_t kk = k;
-  QTT_CUDA(cudaMallocAsync(&X, sizeof(double) * kk * kk, s));
   QTT_CUDA(cudaMallocAsync(&T, sizeof(double) * kk * kk, s));
-  QTT_CUDA(cudaMallocAsync(&norms, sizeof(double) * 2, s));
   QTT_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * kk * kk, s));
   static bool configured = false;
   const int tri_smem = (int)(2 * TRB * (TRB + 1) * sizeof(double));
@@ -907,7 +911,7 @@ int no_truncation_certificate(cudaStream_t s, int k, const double* R, int64_t ld
                                   tri_smem));
     configured = true;
   }
-  trinv_diag_kernel<<<(int)ceil_div(k, TRB), TRB, tri_smem, s>>>(k, R, ldr, X, kk);
+  trinv_diag_kernel<<<(int)ceil_div(k, TRB), 256, tri_smem, s>>>(k, R, ldr, X, kk);
   QTT_CHECK_LAUNCH();
   // Recursive doubling: X12 = -X11 * R12 * X22 for block pairs of size sz.
   for (int sz = TRB; sz < k; sz *= 2) {
@@ -921,6 +925,17 @@ int no_truncation_certificate(cudaStream_t s, int k, const double* R, int64_t ld
       QTT_TRY(dgemm(s, 0, 0, sz, c, sz, -1.0, X11, kk, T, sz, 0.0, X12, kk));
     }
   }
+  QTT_CUDA(cudaFreeAsync(T, s));
+  return kOk;
+}
+
+int no_truncation_certificate(cudaStream_t s, int k, const double* R, int64_t ldr,
+                              const double* delta_dev, double delta_scale, int* ok_dev) {
+  double *X, *norms;
+  const int64_t kk = k;
+  QTT_CUDA(cudaMallocAsync(&X, sizeof(double) * kk * kk, s));
+  QTT_CUDA(cudaMallocAsync(&norms, sizeof(double) * 2, s));
+  QTT_TRY(tri_inverse(s, k, R, ldr, X));
   // ||R||_F (upper triangle of R as stored: caller guarantees zeros below)
   double* Rc;
   QTT_CUDA(cudaMallocAsync(&Rc, sizeof(double) * kk * kk, s));
@@ -931,7 +946,6 @@ int no_truncation_certificate(cudaStream_t s, int k, const double* R, int64_t ld
   QTT_CHECK_LAUNCH();
   QTT_CUDA(cudaFreeAsync(Rc, s));
   QTT_CUDA(cudaFreeAsync(X, s));
-  QTT_CUDA(cudaFreeAsync(T, s));
   QTT_CUDA(cudaFreeAsync(norms, s));
   return kOk;
 }

@@ -33,6 +33,18 @@ int sort_chop(cudaStream_t s, int p, int k, const double* X, int64_t ldx, double
 int no_truncation_certificate(cudaStream_t s, int k, const double* R, int64_t ldr,
                               const double* delta_dev, double delta_scale, int* ok_dev);
 
+// X = R^{-1} for an upper-triangular k x k R (X: k x k, ld k): 64x64 diagonal
+// blocks inverted in shared memory, recursive doubling with DMMA GEMMs.
+int tri_inverse(cudaStream_t s, int k, const double* R, int64_t ldr, double* X);
+
+// CholeskyQR2 (Gram -> Cholesky -> A R^{-1}, twice) for m >= n.  GEMM-bound
+// replacement of the latency-bound Householder panels for well-conditioned
+// tall matrices.  Returns kOk and sets *ok = 1 on success; *ok = 0 when the
+// Cholesky breaks down or the first-pass Q is too far from orthonormal
+// (||Q1^T Q1 - I||_F > 1/4), in which case the caller falls back to Householder.
+int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
+            double* R, int64_t ldr, int* ok);
+
 // Gather columns: dst[:, c] = src[:, perm[c]] for c < cols (device perm).
 int gather_columns(cudaStream_t s, int rows, int cols, const double* src, int64_t lds,
                    const int* perm, double* dst, int64_t ldd);

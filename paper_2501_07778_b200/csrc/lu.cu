@@ -53,32 +53,11 @@ __global__ void __launch_bounds__(256) lu_diag_kernel(int kb, double* __restrict
     const int r = idx % kb, c = idx / kb;
     A[r + (int64_t)c * lda] = S[r][c];
   }
-  // U^{-1}: column c by back substitution (thread c)
-  if (tid < LB) {
-    const int c = tid;
-    for (int r = 0; r < LB; ++r) X[r][c] = 0.0;
-    X[c][c] = 1.0 / S[c][c];
-    for (int i = c - 1; i >= 0; --i) {
-      double acc = 0.0;
-      for (int l = i + 1; l <= c; ++l) acc = fma(S[i][l], X[l][c], acc);
-      X[i][c] = -acc / S[i][i];
-    }
-  }
   __syncthreads();
+  upper_inverse_smem<LB>(S, X, tid);
   for (int idx = tid; idx < LB * LB; idx += blockDim.x) uinv[idx] = X[idx % LB][idx / LB];
   __syncthreads();
-  // L^{-1} (unit lower): column c by forward substitution
-  if (tid < LB) {
-    const int c = tid;
-    for (int r = 0; r < LB; ++r) X[r][c] = 0.0;
-    X[c][c] = 1.0;
-    for (int i = c + 1; i < LB; ++i) {
-      double acc = 0.0;
-      for (int l = c; l < i; ++l) acc = fma(S[i][l], X[l][c], acc);
-      X[i][c] = -acc;
-    }
-  }
-  __syncthreads();
+  unit_lower_inverse_smem<LB>(S, X, tid);
   for (int idx = tid; idx < LB * LB; idx += blockDim.x) linv[idx] = X[idx % LB][idx / LB];
 }
 

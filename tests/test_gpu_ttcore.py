@@ -247,3 +247,27 @@ def test_qr_very_tall_uses_16_wide_panels():
     r = R.cpu().numpy().reshape(n, n).T
     assert np.abs(q @ r - a).max() < 1e-11
     assert np.abs(q.T @ q - np.eye(n)).max() < 1e-12
+
+
+@pytest.mark.parametrize("cond", [1e2, 1e6, 1e12])
+def test_qr_cholqr_path_and_fallback(cond):
+    """n >= 128 tries CholeskyQR2; ill-conditioned inputs fall back to
+    Householder.  Both must give an orthonormal Q and A = QR."""
+    from paper_2501_07778_b200 import _lib
+    import ctypes
+
+    m, n = 1500, 300
+    rng = np.random.default_rng(int(np.log10(cond)))
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    a = (u * np.logspace(0, -np.log10(cond), n)) @ v.T
+    A = torch.tensor(a.ravel(order="F"), device="cuda")
+    Q = torch.zeros(m * n, dtype=torch.float64, device="cuda")
+    R = torch.zeros(n * n, dtype=torch.float64, device="cuda")
+    _lib.call("qtt_qr", ctypes.c_int64(m), ctypes.c_int64(n), _lib.ptr(A), ctypes.c_int64(m),
+              _lib.ptr(Q), ctypes.c_int64(m), _lib.ptr(R), ctypes.c_int64(n), _lib.stream_handle())
+    q = Q.cpu().numpy().reshape(n, m).T
+    r = R.cpu().numpy().reshape(n, n).T
+    assert np.abs(np.tril(r, -1)).max() == 0.0
+    assert np.linalg.norm(q @ r - a) <= 1e-13 * np.linalg.norm(a)
+    assert np.abs(q.T @ q - np.eye(n)).max() < 1e-12
