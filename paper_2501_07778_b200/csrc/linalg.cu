@@ -658,7 +658,7 @@ int set_identity(cudaStream_t s, int rows, int cols, double* A, int64_t lda) {
 }
 
 // Side stream for the look-ahead panel factorisation (one per process).
-static cudaStream_t side_stream() {
+cudaStream_t side_stream() {
   static cudaStream_t st = nullptr;
   if (!st) {
     // highest priority: the panel (critical path) is scheduled ahead of the

@@ -45,6 +45,10 @@ int tri_inverse(cudaStream_t s, int k, const double* R, int64_t ldr, double* X);
 int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
             double* R, int64_t ldr, int* ok);
 
+// Process-wide high-priority side stream used for look-ahead factorisation
+// of the next panel / diagonal block while the trailing update runs.
+cudaStream_t side_stream();
+
 // Gather columns: dst[:, c] = src[:, perm[c]] for c < cols (device perm).
 int gather_columns(cudaStream_t s, int rows, int cols, const double* src, int64_t lds,
                    const int* perm, double* dst, int64_t ldd);

@@ -119,35 +119,53 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
   QTT_TRY(copy_matrix(s, N, N, M, ldm, A, ld));
   QTT_TRY(frob_norm(s, ld * N, A, nrm + 2));  // ||M||_F before A is factorised
   QTT_CUDA(cudaMemcpyAsync(A + ld * N, b, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
-  // ---- forward elimination on [M | b]
+  // ---- forward elimination on [M | b], with look-ahead: after the panel
+  // solves of block k only the next block column is updated, the next
+  // diagonal block is factorised on the side stream while the rest of the
+  // Schur complement is updated here.
+  static cudaEvent_t ev_col = nullptr, ev_diag = nullptr;
+  if (!ev_col) {
+    QTT_CUDA(cudaEventCreateWithFlags(&ev_col, cudaEventDisableTiming));
+    QTT_CUDA(cudaEventCreateWithFlags(&ev_diag, cudaEventDisableTiming));
+  }
+  cudaStream_t sb = side_stream();
+  double *Lp, *Up;
+  QTT_CUDA(cudaMallocAsync(&Lp, sizeof(double) * ld * LB, s));
+  QTT_CUDA(cudaMallocAsync(&Up, sizeof(double) * (int64_t)LB * (N + 1), s));
+  lu_diag_kernel<<<1, 256, kLuSmem, s>>>(std::min(LB, N), A, ld, linv, uinv, bad);
+  QTT_CHECK_LAUNCH();
   for (int kb0 = 0, blk = 0; kb0 < N; kb0 += LB, ++blk) {
     const int kb = std::min(LB, N - kb0);
-    double* A11 = A + kb0 + (int64_t)kb0 * ld;
-    lu_diag_kernel<<<1, 256, kLuSmem, s>>>(kb, A11, ld, linv + (int64_t)blk * LB * LB,
-                                     uinv + (int64_t)blk * LB * LB, bad);
-    QTT_CHECK_LAUNCH();
     const int m2 = N - kb0 - kb;      // rows below
     const int n2 = N + 1 - kb0 - kb;  // columns right (incl. rhs)
-    if (m2 > 0) {
-      // L21 = A21 U11^{-1}
-      double* A21 = A + (kb0 + kb) + (int64_t)kb0 * ld;
-      QTT_TRY(dgemm(s, 0, 0, m2, kb, kb, 1.0, A21, ld, uinv + (int64_t)blk * LB * LB, LB, 0.0, tmp,
-                    m2));
-      QTT_TRY(copy_matrix(s, m2, kb, tmp, m2, A21, ld));
+    double* A21 = A + (kb0 + kb) + (int64_t)kb0 * ld;
+    double* A12 = A + kb0 + (int64_t)(kb0 + kb) * ld;
+    if (m2 > 0)  // L21 = A21 U11^{-1}
+      QTT_TRY(dgemm(s, 0, 0, m2, kb, kb, 1.0, A21, ld, uinv + (int64_t)blk * LB * LB, LB, 0.0, Lp, m2));
+    // U12 = L11^{-1} A12 (includes the rhs column)
+    QTT_TRY(dgemm(s, 0, 0, kb, n2, kb, 1.0, linv + (int64_t)blk * LB * LB, LB, A12, ld, 0.0, Up, kb));
+    const int kb1 = m2 > 0 ? std::min(LB, m2) : 0;
+    if (kb1 > 0) {
+      double* A22n = A + (kb0 + kb) + (int64_t)(kb0 + kb) * ld;  // next block column
+      QTT_TRY(dgemm(s, 0, 0, m2, kb1, kb, -1.0, Lp, m2, Up, kb, 1.0, A22n, ld));
+      QTT_CUDA(cudaEventRecord(ev_col, s));
+      QTT_CUDA(cudaStreamWaitEvent(sb, ev_col, 0));
+      lu_diag_kernel<<<1, 256, kLuSmem, sb>>>(kb1, A22n, ld, linv + (int64_t)(blk + 1) * LB * LB,
+                                              uinv + (int64_t)(blk + 1) * LB * LB, bad);
+      QTT_CHECK_LAUNCH();
+      QTT_CUDA(cudaEventRecord(ev_diag, sb));
+      const int rest = n2 - kb1;
+      if (rest > 0)
+        QTT_TRY(dgemm(s, 0, 0, m2, rest, kb, -1.0, Lp, m2, Up + (int64_t)kb1 * kb, kb, 1.0,
+                      A22n + (int64_t)kb1 * ld, ld));
     }
-    if (n2 > 0) {
-      // U12 = L11^{-1} A12 (includes the rhs column)
-      double* A12 = A + kb0 + (int64_t)(kb0 + kb) * ld;
-      QTT_TRY(dgemm(s, 0, 0, kb, n2, kb, 1.0, linv + (int64_t)blk * LB * LB, LB, A12, ld, 0.0, tmp,
-                    kb));
-      QTT_TRY(copy_matrix(s, kb, n2, tmp, kb, A12, ld));
-      if (m2 > 0) {
-        double* A21 = A + (kb0 + kb) + (int64_t)kb0 * ld;
-        double* A22 = A + (kb0 + kb) + (int64_t)(kb0 + kb) * ld;
-        QTT_TRY(dgemm(s, 0, 0, m2, n2, kb, -1.0, A21, ld, A12, ld, 1.0, A22, ld));
-      }
-    }
+    // keep L21 / U12 in A for the back substitution and the refinement
+    if (m2 > 0) QTT_TRY(copy_matrix(s, m2, kb, Lp, m2, A21, ld));
+    QTT_TRY(copy_matrix(s, kb, n2, Up, kb, A12, ld));
+    if (kb1 > 0) QTT_CUDA(cudaStreamWaitEvent(s, ev_diag, 0));
   }
+  QTT_CUDA(cudaFreeAsync(Lp, s));
+  QTT_CUDA(cudaFreeAsync(Up, s));
   // ---- back substitution U x = y (y = last column)
   double* y = A + ld * N;
   for (int blk = nblk - 1; blk >= 0; --blk) {
