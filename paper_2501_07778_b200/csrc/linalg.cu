@@ -914,9 +914,26 @@ int tri_inverse(cudaStream_t s, int k, const double* R, int64_t ldr, double* X) 
   trinv_diag_kernel<<<(int)ceil_div(k, TRB), 256, tri_smem, s>>>(k, R, ldr, X, kk);
   QTT_CHECK_LAUNCH();
   // Recursive doubling: X12 = -X11 * R12 * X22 for block pairs of size sz.
+  // All full pairs of a level have the same shape and a constant stride
+  // 2 sz (1 + ld) along the diagonal: one batched GEMM per product and level;
+  // a trailing partial pair (c < sz) is issued separately.
   for (int sz = TRB; sz < k; sz *= 2) {
-    for (int b = 0; b + sz < k; b += 2 * sz) {
-      const int c = std::min(sz, k - b - sz);
+    const int full = (k / (2 * sz));  // pairs with c == sz
+    if (full > 0) {
+      GemmArgs g1{sz, sz, sz, 0, 0, 1.0, 0.0,
+                  R + (int64_t)sz * ldr, ldr, 2 * (int64_t)sz * (1 + ldr),
+                  X + sz + (int64_t)sz * kk, kk, 2 * (int64_t)sz * (1 + kk),
+                  T, sz, (int64_t)sz * sz, full};
+      QTT_TRY(gemm(g1, s));
+      GemmArgs g2{sz, sz, sz, 0, 0, -1.0, 0.0,
+                  X, kk, 2 * (int64_t)sz * (1 + kk),
+                  T, sz, (int64_t)sz * sz,
+                  X + (int64_t)sz * kk, kk, 2 * (int64_t)sz * (1 + kk), full};
+      QTT_TRY(gemm(g2, s));
+    }
+    const int b = full * 2 * sz;
+    if (b + sz < k) {
+      const int c = k - b - sz;  // < sz
       const double* R12 = R + b + (int64_t)(b + sz) * ldr;
       const double* X22 = X + (b + sz) + (int64_t)(b + sz) * kk;
       const double* X11 = X + b + (int64_t)b * kk;
