@@ -37,31 +37,42 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* __restr
     S[r][c] = (r < kb && c < kb) ? G[r + (int64_t)c * ldg] : (r == c ? 1.0 : 0.0);
   }
   __syncthreads();
-  for (int j = 0; j < kb; ++j) {
-    const double piv = S[j][j];
-    if (!(piv > 0.0) || !isfinite(piv)) {
-      if (tid == 0) atomicExch(bad, 1);
-      return;  // uniform: every thread reads the same pivot
-    }
-    const double d = sqrt(piv);
-    __syncthreads();
-    for (int c = j + tid; c < kb; c += blockDim.x) S[j][c] = (c == j) ? d : S[j][c] / d;
-    __syncthreads();
-    const int rem = kb - j - 1;
-    for (int idx = tid; idx < rem * rem; idx += blockDim.x) {
-      const int r = j + 1 + idx % rem, c = j + 1 + idx / rem;
-      if (r <= c) S[r][c] = fma(-S[j][r], S[j][c], S[r][c]);
-    }
-    __syncthreads();
-  }
+  crout_factor64<true>(S, &X[0][0], kb, bad);
   for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
     const int r = idx % kb, c = idx / kb;
     G[r + (int64_t)c * ldg] = (r <= c) ? S[r][c] : 0.0;
   }
+}
+
+// Panel solve of the blocked Cholesky: B <- R11^{-T} B for the kb x ncols
+// block row B (ld ldb), R11 the kb x kb upper factor.  One thread per column,
+// forward substitution with R11 in shared memory (broadcast reads) and the
+// column kept in a transposed shared-memory slab (conflict-free).
+constexpr int TRSM_COLS = 128;
+constexpr int kTrsmSmem = (CB * (CB + 1) + CB * (TRSM_COLS + 1)) * sizeof(double);
+__global__ void __launch_bounds__(TRSM_COLS) trsm_upper_t_kernel(int kb, const double* __restrict__ R,
+                                                                  int64_t ldr, double* __restrict__ B,
+                                                                  int64_t ldb, int ncols) {
+  extern __shared__ double trsm_sm[];
+  double (*Rs)[CB + 1] = reinterpret_cast<double (*)[CB + 1]>(trsm_sm);
+  double (*Xs)[TRSM_COLS + 1] = reinterpret_cast<double (*)[TRSM_COLS + 1]>(trsm_sm + CB * (CB + 1));
+  for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
+    const int r = idx % kb, c = idx / kb;
+    Rs[r][c] = R[r + (int64_t)c * ldr];
+  }
+  const int col = blockIdx.x * TRSM_COLS + threadIdx.x;
+  const bool active = col < ncols;
+  if (active)
+    for (int i = 0; i < kb; ++i) Xs[i][threadIdx.x] = B[i + (int64_t)col * ldb];
   __syncthreads();
-  upper_inverse_smem<CB>(S, X, tid);
-  __syncthreads();
-  for (int idx = tid; idx < CB * CB; idx += blockDim.x) rinv[idx] = X[idx % CB][idx / CB];
+  if (active) {
+    for (int i = 0; i < kb; ++i) {
+      double acc = Xs[i][threadIdx.x];
+      for (int l = 0; l < i; ++l) acc = fma(-Rs[l][i], Xs[l][threadIdx.x], acc);
+      Xs[i][threadIdx.x] = acc / Rs[i][i];
+    }
+    for (int i = 0; i < kb; ++i) B[i + (int64_t)col * ldb] = Xs[i][threadIdx.x];
+  }
 }
 
 // partial sums of squares of (G - I) for the orthogonality certificate
@@ -100,6 +111,8 @@ int chol_upper(cudaStream_t s, int n, double* G, int64_t ldg, double* rinv, doub
   if (!configured) {
     QTT_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kCholSmem));
+    QTT_CUDA(cudaFuncSetAttribute(trsm_upper_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kTrsmSmem));
     configured = true;
   }
   for (int k0 = 0; k0 < n; k0 += CB) {
@@ -109,10 +122,11 @@ int chol_upper(cudaStream_t s, int n, double* G, int64_t ldg, double* rinv, doub
     QTT_CHECK_LAUNCH();
     const int rest = n - k0 - kb;
     if (rest <= 0) break;
-    // R12 = R11^{-T} G12  (kb x rest), written back into G12
+    // R12 = R11^{-T} G12  (kb x rest), in place by forward substitution
     double* G12 = G + k0 + (int64_t)(k0 + kb) * ldg;
-    QTT_TRY(dgemm(s, 1, 0, kb, rest, kb, 1.0, rinv, CB, G12, ldg, 0.0, tmp, kb));
-    QTT_TRY(copy_matrix(s, kb, rest, tmp, kb, G12, ldg));
+    trsm_upper_t_kernel<<<(int)ceil_div(rest, TRSM_COLS), TRSM_COLS, kTrsmSmem, s>>>(kb, Gkk, ldg,
+                                                                                    G12, ldg, rest);
+    QTT_CHECK_LAUNCH();
     // G22 -= R12^T R12 (full square update; only the upper part is used)
     double* G22 = G + (k0 + kb) + (int64_t)(k0 + kb) * ldg;
     QTT_TRY(dgemm(s, 1, 0, rest, rest, kb, -1.0, G12, ldg, G12, ldg, 1.0, G22, ldg));

@@ -64,9 +64,17 @@ __device__ __forceinline__ void upper_inverse_smem(double (*S)[B + 1], double (*
   for (int r = part; r < B; r += 4) X[r][c] = 0.0;
   __syncthreads();
   for (int i = B - 1; i >= 0; --i) {
-    double acc = 0.0;
-    if (c > i)
-      for (int l = i + 1 + part; l <= c; l += 4) acc = fma(S[i][l], X[l][c], acc);
+    double acc = 0.0, acc2 = 0.0;
+    if (c > i) {
+      int l = i + 1 + part;
+#pragma unroll 2
+      for (; l + 4 <= c; l += 8) {
+        acc = fma(S[i][l], X[l][c], acc);
+        acc2 = fma(S[i][l + 4], X[l + 4][c], acc2);
+      }
+      if (l <= c) acc = fma(S[i][l], X[l][c], acc);
+    }
+    acc += acc2;
     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
     acc += __shfl_xor_sync(0xffffffffu, acc, 2);
     if (part == 0 && c >= i) X[i][c] = (c == i) ? 1.0 / S[i][i] : -acc / S[i][i];
@@ -89,6 +97,65 @@ __device__ __forceinline__ void unit_lower_inverse_smem(double (*S)[B + 1], doub
     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
     acc += __shfl_xor_sync(0xffffffffu, acc, 2);
     if (part == 0 && c <= i) X[i][c] = (c == i) ? 1.0 : -acc;
+    __syncthreads();
+  }
+}
+
+// Left-looking (Crout) factorisation of the leading kb x kb part of a 64 x 64
+// shared-memory block, 256 threads, two barriers per step.  Step j computes
+// every entry of row j (and, for LU, column j) as ONE dot product of length j
+// against the already finished rows/columns, two lanes per entry:
+//   CHOL: R[j][c] = (G[j][c] - sum_l R[l][j] R[l][c]) / R[j][j],  c >= j
+//   LU  : U[j][c] =  A[j][c] - sum_l L[j][l] U[l][c],            c >= j
+//         L[r][j] = (A[r][j] - sum_l L[r][l] U[l][j]) / U[j][j], r >  j
+// `tmp` needs 128 doubles of shared memory.  *bad is set on a non-positive
+// (CHOL) or zero (LU) pivot.  For CHOL the strictly lower part is zeroed.
+template <bool CHOL>
+__device__ __forceinline__ void crout_factor64(double (*S)[65], double* tmp, int kb, int* bad) {
+  const int tid = threadIdx.x, item = tid >> 1, half = tid & 1;
+  for (int j = 0; j < kb; ++j) {
+    const int nrow = kb - j;                 // row items c = j .. kb-1
+    const int ncol = CHOL ? 0 : kb - j - 1;  // column items r = j+1 .. kb-1
+    double acc = 0.0, acc2 = 0.0;
+    if (item < nrow) {
+      const int c = j + item;
+      int l = half;
+#pragma unroll 2
+      for (; l + 2 < j; l += 4) {
+        acc = fma(CHOL ? S[l][j] : S[j][l], S[l][c], acc);
+        acc2 = fma(CHOL ? S[l + 2][j] : S[j][l + 2], S[l + 2][c], acc2);
+      }
+      if (l < j) acc = fma(CHOL ? S[l][j] : S[j][l], S[l][c], acc);
+    } else if (item < nrow + ncol) {
+      const int r = j + 1 + (item - nrow);
+      int l = half;
+#pragma unroll 2
+      for (; l + 2 < j; l += 4) {
+        acc = fma(S[r][l], S[l][j], acc);
+        acc2 = fma(S[r][l + 2], S[l + 2][j], acc2);
+      }
+      if (l < j) acc = fma(S[r][l], S[l][j], acc);
+    }
+    acc += acc2;
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (half == 0 && item < nrow + ncol) {
+      const double base = item < nrow ? S[j][j + item] : S[j + 1 + (item - nrow)][j];
+      tmp[item] = base - acc;
+    }
+    __syncthreads();
+    const double piv = tmp[0];
+    if (tid == 0 && (CHOL ? !(piv > 0.0) : !(fabs(piv) > 0.0))) atomicExch(bad, 1);
+    if (half == 0 && item < nrow + ncol) {
+      if (item < nrow) S[j][j + item] = CHOL ? tmp[item] / sqrt(piv) : tmp[item];
+      else S[j + 1 + (item - nrow)][j] = tmp[item] / piv;
+    }
+    __syncthreads();
+  }
+  if (CHOL) {
+    for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
+      const int r = idx % kb, c = idx / kb;
+      if (r > c) S[r][c] = 0.0;
+    }
     __syncthreads();
   }
 }

@@ -35,20 +35,7 @@ __global__ void __launch_bounds__(256) lu_diag_kernel(int kb, double* __restrict
     S[r][c] = (r < kb && c < kb) ? A[r + (int64_t)c * lda] : (r == c ? 1.0 : 0.0);
   }
   __syncthreads();
-  for (int j = 0; j < kb; ++j) {
-    const double piv = S[j][j];
-    if (tid == 0 && !(fabs(piv) > 0.0)) atomicExch(bad, 1);
-    __syncthreads();
-    const double inv = 1.0 / piv;
-    for (int r = j + 1 + tid; r < kb; r += blockDim.x) S[r][j] *= inv;
-    __syncthreads();
-    const int rem = kb - j - 1;
-    for (int idx = tid; idx < rem * rem; idx += blockDim.x) {
-      const int r = j + 1 + idx % rem, c = j + 1 + idx / rem;
-      S[r][c] = fma(-S[r][j], S[j][c], S[r][c]);
-    }
-    __syncthreads();
-  }
+  crout_factor64<false>(S, &X[0][0], kb, bad);
   for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
     const int r = idx % kb, c = idx / kb;
     A[r + (int64_t)c * lda] = S[r][c];
