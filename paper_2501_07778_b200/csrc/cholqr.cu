@@ -20,58 +20,68 @@ namespace qtt {
 namespace {
 
 constexpr int CB = 64;  // Cholesky block
-constexpr int kCholSmem = 2 * CB * (CB + 1) * sizeof(double);
 constexpr int kDefectParts = 296;
 
-// Upper Cholesky of the kb x kb diagonal block (in place, lower part zeroed)
-// and the inverse of the factor into rinv (CB x CB, zero padded).
-__global__ void __launch_bounds__(256) potrf_diag_kernel(int kb, double* __restrict__ G,
-                                                         int64_t ldg, double* __restrict__ rinv,
+// One block step of the blocked Cholesky, fused: every CTA factors the
+// kb x kb diagonal block G11 = R11^T R11 in registers (redundantly; it is a
+// few microseconds and saves a launch + a dependency), CTA 0 writes R11 to
+// `rblk` (64 x 64, ld 64; copied into G after the last step, because other
+// CTAs may still be reading G11), and each CTA solves 64 columns of the
+// block row in place, G12 <- R11^{-T} G12, by forward substitution with four
+// lanes per column: the pivot entry travels by warp shuffle, no barriers.
+__global__ void __launch_bounds__(256) chol_panel_kernel(int kb, const double* __restrict__ G11,
+                                                         int64_t ldg, double* __restrict__ rblk,
+                                                         double* __restrict__ G12, int rest,
                                                          int* __restrict__ bad) {
-  extern __shared__ double ch_sm[];
-  double (*S)[CB + 1] = reinterpret_cast<double (*)[CB + 1]>(ch_sm);
-  double (*X)[CB + 1] = reinterpret_cast<double (*)[CB + 1]>(ch_sm + CB * (CB + 1));
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < CB * CB; idx += blockDim.x) {
-    const int r = idx % CB, c = idx / CB;
-    S[r][c] = (r < kb && c < kb) ? G[r + (int64_t)c * ldg] : (r == c ? 1.0 : 0.0);
+  __shared__ double S[kBlk][kBlk + 1];
+  __shared__ double line[256];
+  __shared__ double dinv[kBlk];
+  double a[16];
+  blk_load(a, G11, ldg, kb);
+  blk_factor<true>(a, line, bad);
+  if (blockIdx.x == 0) blk_store(a, rblk, kBlk, kBlk);
+  const int col = blockIdx.x * kBlk + blk_col();
+  if (blockIdx.x * kBlk >= rest) return;
+  blk_to_smem(a, S);
+  __syncthreads();
+  if (threadIdx.x < kBlk) dinv[threadIdx.x] = 1.0 / S[threadIdx.x][threadIdx.x];
+  const int part = blk_part(), lane = threadIdx.x & 31;
+  const bool act = col < rest;
+  double x[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int i = part + 4 * q;
+    x[q] = (act && i < kb) ? G12[i + (int64_t)col * ldg] : 0.0;
   }
   __syncthreads();
-  crout_factor64<true>(S, &X[0][0], kb, bad);
-  for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
-    const int r = idx % kb, c = idx / kb;
-    G[r + (int64_t)c * ldg] = (r <= c) ? S[r][c] : 0.0;
+#pragma unroll
+  for (int j = 0; j < kBlk; ++j) {
+    const int qj = j >> 2, pj = j & 3;
+    const double v = x[qj] * dinv[j];
+    const double xj = __shfl_sync(0xffffffffu, v, (lane & ~3) | pj);
+    if (part == pj) x[qj] = v;
+#pragma unroll
+    for (int q = qj; q < 16; ++q)
+      if (part + 4 * q > j) x[q] = fma(-S[j][part + 4 * q], xj, x[q]);
+  }
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = part + 4 * q;
+      if (i < kb) G12[i + (int64_t)col * ldg] = x[q];
+    }
   }
 }
 
-// Panel solve of the blocked Cholesky: B <- R11^{-T} B for the kb x ncols
-// block row B (ld ldb), R11 the kb x kb upper factor.  One thread per column,
-// forward substitution with R11 in shared memory (broadcast reads) and the
-// column kept in a transposed shared-memory slab (conflict-free).
-constexpr int TRSM_COLS = 128;
-constexpr int kTrsmSmem = (CB * (CB + 1) + CB * (TRSM_COLS + 1)) * sizeof(double);
-__global__ void __launch_bounds__(TRSM_COLS) trsm_upper_t_kernel(int kb, const double* __restrict__ R,
-                                                                  int64_t ldr, double* __restrict__ B,
-                                                                  int64_t ldb, int ncols) {
-  extern __shared__ double trsm_sm[];
-  double (*Rs)[CB + 1] = reinterpret_cast<double (*)[CB + 1]>(trsm_sm);
-  double (*Xs)[TRSM_COLS + 1] = reinterpret_cast<double (*)[TRSM_COLS + 1]>(trsm_sm + CB * (CB + 1));
+// G(diag block b) <- rblk[b] (upper incl. diagonal; strictly lower zero).
+__global__ void __launch_bounds__(256) chol_diag_writeback_kernel(int n, const double* __restrict__ rblk,
+                                                                  double* __restrict__ G, int64_t ldg) {
+  const int b0 = blockIdx.x * kBlk;
+  const int kb = min(kBlk, n - b0);
+  const double* src = rblk + (int64_t)blockIdx.x * kBlk * kBlk;
   for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
     const int r = idx % kb, c = idx / kb;
-    Rs[r][c] = R[r + (int64_t)c * ldr];
-  }
-  const int col = blockIdx.x * TRSM_COLS + threadIdx.x;
-  const bool active = col < ncols;
-  if (active)
-    for (int i = 0; i < kb; ++i) Xs[i][threadIdx.x] = B[i + (int64_t)col * ldb];
-  __syncthreads();
-  if (active) {
-    for (int i = 0; i < kb; ++i) {
-      double acc = Xs[i][threadIdx.x];
-      for (int l = 0; l < i; ++l) acc = fma(-Rs[l][i], Xs[l][threadIdx.x], acc);
-      Xs[i][threadIdx.x] = acc / Rs[i][i];
-    }
-    for (int i = 0; i < kb; ++i) B[i + (int64_t)col * ldb] = Xs[i][threadIdx.x];
+    G[(b0 + r) + (int64_t)(b0 + c) * ldg] = src[r + c * kBlk];
   }
 }
 
@@ -104,29 +114,19 @@ __global__ void sum_parts_kernel(int n, const double* __restrict__ part, double*
   }
 }
 
-// Blocked right-looking upper Cholesky G = R^T R (in place).
-int chol_upper(cudaStream_t s, int n, double* G, int64_t ldg, double* rinv, double* tmp,
-               int* bad) {
-  static bool configured = false;
-  if (!configured) {
-    QTT_CUDA(cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kCholSmem));
-    QTT_CUDA(cudaFuncSetAttribute(trsm_upper_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kTrsmSmem));
-    configured = true;
-  }
-  for (int k0 = 0; k0 < n; k0 += CB) {
+// Blocked right-looking upper Cholesky G = R^T R (in place).  rblk: scratch
+// for the ceil(n/64) diagonal factors (64 x 64 each).
+int chol_upper(cudaStream_t s, int n, double* G, int64_t ldg, double* rblk, int* bad) {
+  int nblk = 0;
+  for (int k0 = 0; k0 < n; k0 += CB, ++nblk) {
     const int kb = std::min(CB, n - k0);
-    double* Gkk = G + k0 + (int64_t)k0 * ldg;
-    potrf_diag_kernel<<<1, 256, kCholSmem, s>>>(kb, Gkk, ldg, rinv, bad);
-    QTT_CHECK_LAUNCH();
     const int rest = n - k0 - kb;
-    if (rest <= 0) break;
-    // R12 = R11^{-T} G12  (kb x rest), in place by forward substitution
+    const double* Gkk = G + k0 + (int64_t)k0 * ldg;
     double* G12 = G + k0 + (int64_t)(k0 + kb) * ldg;
-    trsm_upper_t_kernel<<<(int)ceil_div(rest, TRSM_COLS), TRSM_COLS, kTrsmSmem, s>>>(kb, Gkk, ldg,
-                                                                                    G12, ldg, rest);
+    chol_panel_kernel<<<std::max(1, (int)ceil_div(rest, CB)), 256, 0, s>>>(
+        kb, Gkk, ldg, rblk + (int64_t)nblk * CB * CB, G12, rest, bad);
     QTT_CHECK_LAUNCH();
+    if (rest <= 0) continue;
     // G22 -= R12^T R12 (full square update; only the upper part is used)
     double* G22 = G + (k0 + kb) + (int64_t)(k0 + kb) * ldg;
     QTT_TRY(dgemm(s, 1, 0, rest, rest, kb, -1.0, G12, ldg, G12, ldg, 1.0, G22, ldg));
@@ -134,6 +134,8 @@ int chol_upper(cudaStream_t s, int n, double* G, int64_t ldg, double* rinv, doub
     QTT_CUDA(cudaMemset2DAsync(G + (k0 + kb) + (int64_t)k0 * ldg, sizeof(double) * ldg, 0,
                                sizeof(double) * rest, kb, s));
   }
+  chol_diag_writeback_kernel<<<nblk, 256, 0, s>>>(n, rblk, G, ldg);
+  QTT_CHECK_LAUNCH();
   return kOk;
 }
 
@@ -144,14 +146,13 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
   *ok = 0;
   if (m < n || n <= 0) return kOk;
   const int64_t nn = n;
-  double *G, *R1, *Ri, *Q1, *rinv, *tmp, *scal, *parts;
+  double *G, *R1, *Ri, *Q1, *rblk, *scal, *parts;
   int* bad;
   QTT_CUDA(cudaMallocAsync(&G, sizeof(double) * nn * nn, s));
   QTT_CUDA(cudaMallocAsync(&R1, sizeof(double) * nn * nn, s));
   QTT_CUDA(cudaMallocAsync(&Ri, sizeof(double) * nn * nn, s));
   QTT_CUDA(cudaMallocAsync(&Q1, sizeof(double) * (int64_t)m * nn, s));
-  QTT_CUDA(cudaMallocAsync(&rinv, sizeof(double) * CB * CB, s));
-  QTT_CUDA(cudaMallocAsync(&tmp, sizeof(double) * CB * nn, s));
+  QTT_CUDA(cudaMallocAsync(&rblk, sizeof(double) * CB * CB * ceil_div(nn, CB), s));
   QTT_CUDA(cudaMallocAsync(&scal, sizeof(double) * 4, s));
   QTT_CUDA(cudaMallocAsync(&parts, sizeof(double) * kDefectParts, s));
   QTT_CUDA(cudaMallocAsync(&bad, sizeof(int), s));
@@ -160,7 +161,7 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
   do {
     // pass 1: G = A^T A = R1^T R1, Q1 = A R1^{-1}
     if ((status = dgemm(s, 1, 0, n, n, m, 1.0, A, lda, A, lda, 0.0, G, nn)) != kOk) break;
-    if ((status = chol_upper(s, n, G, nn, rinv, tmp, bad)) != kOk) break;
+    if ((status = chol_upper(s, n, G, nn, rblk, bad)) != kOk) break;
     int hbad = 0;
     QTT_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
     QTT_CUDA(cudaStreamSynchronize(s));
@@ -179,7 +180,7 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
     QTT_CUDA(cudaStreamSynchronize(s));
     if (getenv("QTT_QR_DEBUG")) fprintf(stderr, "[cholqr2] m=%d n=%d defect=%.3e\n", m, n, std::sqrt(defect));
     if (!(std::sqrt(defect) <= 0.25)) break;
-    if ((status = chol_upper(s, n, G, nn, rinv, tmp, bad)) != kOk) break;
+    if ((status = chol_upper(s, n, G, nn, rblk, bad)) != kOk) break;
     QTT_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
     QTT_CUDA(cudaStreamSynchronize(s));
     if (hbad) break;
@@ -193,8 +194,7 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
   QTT_CUDA(cudaFreeAsync(R1, s));
   QTT_CUDA(cudaFreeAsync(Ri, s));
   QTT_CUDA(cudaFreeAsync(Q1, s));
-  QTT_CUDA(cudaFreeAsync(rinv, s));
-  QTT_CUDA(cudaFreeAsync(tmp, s));
+  QTT_CUDA(cudaFreeAsync(rblk, s));
   QTT_CUDA(cudaFreeAsync(scal, s));
   QTT_CUDA(cudaFreeAsync(parts, s));
   QTT_CUDA(cudaFreeAsync(bad, s));

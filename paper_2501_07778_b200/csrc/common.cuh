@@ -53,113 +53,6 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// X = S^{-1} for an upper-triangular B x B block in shared memory (B = 64,
-// 256 threads): rows bottom-up, all columns of a row in one step, 4 lanes per
-// column splitting the dot product.  Replaces column-per-thread substitution
-// (B^2/2 dependent shared-memory FMAs per thread).
-template <int B>
-__device__ __forceinline__ void upper_inverse_smem(double (*S)[B + 1], double (*X)[B + 1], int tid) {
-  static_assert(B * 4 == 256, "256 threads per block");
-  const int c = tid >> 2, part = tid & 3;
-  for (int r = part; r < B; r += 4) X[r][c] = 0.0;
-  __syncthreads();
-  for (int i = B - 1; i >= 0; --i) {
-    double acc = 0.0, acc2 = 0.0;
-    if (c > i) {
-      int l = i + 1 + part;
-#pragma unroll 2
-      for (; l + 4 <= c; l += 8) {
-        acc = fma(S[i][l], X[l][c], acc);
-        acc2 = fma(S[i][l + 4], X[l + 4][c], acc2);
-      }
-      if (l <= c) acc = fma(S[i][l], X[l][c], acc);
-    }
-    acc += acc2;
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    if (part == 0 && c >= i) X[i][c] = (c == i) ? 1.0 / S[i][i] : -acc / S[i][i];
-    __syncthreads();
-  }
-}
-
-// X = L^{-1} for the unit lower-triangular part of S (diagonal taken as 1).
-template <int B>
-__device__ __forceinline__ void unit_lower_inverse_smem(double (*S)[B + 1], double (*X)[B + 1],
-                                                        int tid) {
-  static_assert(B * 4 == 256, "256 threads per block");
-  const int c = tid >> 2, part = tid & 3;
-  for (int r = part; r < B; r += 4) X[r][c] = 0.0;
-  __syncthreads();
-  for (int i = 0; i < B; ++i) {
-    double acc = 0.0;
-    if (c < i)
-      for (int l = c + part; l < i; l += 4) acc = fma(S[i][l], X[l][c], acc);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    if (part == 0 && c <= i) X[i][c] = (c == i) ? 1.0 : -acc;
-    __syncthreads();
-  }
-}
-
-// Left-looking (Crout) factorisation of the leading kb x kb part of a 64 x 64
-// shared-memory block, 256 threads, two barriers per step.  Step j computes
-// every entry of row j (and, for LU, column j) as ONE dot product of length j
-// against the already finished rows/columns, two lanes per entry:
-//   CHOL: R[j][c] = (G[j][c] - sum_l R[l][j] R[l][c]) / R[j][j],  c >= j
-//   LU  : U[j][c] =  A[j][c] - sum_l L[j][l] U[l][c],            c >= j
-//         L[r][j] = (A[r][j] - sum_l L[r][l] U[l][j]) / U[j][j], r >  j
-// `tmp` needs 128 doubles of shared memory.  *bad is set on a non-positive
-// (CHOL) or zero (LU) pivot.  For CHOL the strictly lower part is zeroed.
-template <bool CHOL>
-__device__ __forceinline__ void crout_factor64(double (*S)[65], double* tmp, int kb, int* bad) {
-  const int tid = threadIdx.x, item = tid >> 1, half = tid & 1;
-  for (int j = 0; j < kb; ++j) {
-    const int nrow = kb - j;                 // row items c = j .. kb-1
-    const int ncol = CHOL ? 0 : kb - j - 1;  // column items r = j+1 .. kb-1
-    double acc = 0.0, acc2 = 0.0;
-    if (item < nrow) {
-      const int c = j + item;
-      int l = half;
-#pragma unroll 2
-      for (; l + 2 < j; l += 4) {
-        acc = fma(CHOL ? S[l][j] : S[j][l], S[l][c], acc);
-        acc2 = fma(CHOL ? S[l + 2][j] : S[j][l + 2], S[l + 2][c], acc2);
-      }
-      if (l < j) acc = fma(CHOL ? S[l][j] : S[j][l], S[l][c], acc);
-    } else if (item < nrow + ncol) {
-      const int r = j + 1 + (item - nrow);
-      int l = half;
-#pragma unroll 2
-      for (; l + 2 < j; l += 4) {
-        acc = fma(S[r][l], S[l][j], acc);
-        acc2 = fma(S[r][l + 2], S[l + 2][j], acc2);
-      }
-      if (l < j) acc = fma(S[r][l], S[l][j], acc);
-    }
-    acc += acc2;
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    if (half == 0 && item < nrow + ncol) {
-      const double base = item < nrow ? S[j][j + item] : S[j + 1 + (item - nrow)][j];
-      tmp[item] = base - acc;
-    }
-    __syncthreads();
-    const double piv = tmp[0];
-    if (tid == 0 && (CHOL ? !(piv > 0.0) : !(fabs(piv) > 0.0))) atomicExch(bad, 1);
-    if (half == 0 && item < nrow + ncol) {
-      if (item < nrow) S[j][j + item] = CHOL ? tmp[item] / sqrt(piv) : tmp[item];
-      else S[j + 1 + (item - nrow)][j] = tmp[item] / piv;
-    }
-    __syncthreads();
-  }
-  if (CHOL) {
-    for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
-      const int r = idx % kb, c = idx / kb;
-      if (r > c) S[r][c] = 0.0;
-    }
-    __syncthreads();
-  }
-}
-
 __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) {
   return (a + b - 1) / b;
 }
@@ -173,6 +66,136 @@ inline int num_sms() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+// ------------------------------------------------- 64 x 64 register blocks
+// The diagonal-block kernels of the blocked Cholesky / LU / triangular
+// inverse keep a 64 x 64 block in the registers of 256 threads: thread t
+// holds column c = t >> 2, rows part + 4q (part = t & 3, q = 0..15).  Each
+// elimination step is right-looking (one rank-1 update of at most 16 entries
+// per thread) and exchanges the pivot row / column through a double-buffered
+// shared-memory line, so a step costs ONE block barrier and its critical
+// path is store -> barrier -> load -> fma.  The 64 steps are fully unrolled
+// so every register index is a compile-time constant.
+constexpr int kBlk = 64;
+__device__ __forceinline__ int blk_col() { return threadIdx.x >> 2; }
+__device__ __forceinline__ int blk_part() { return threadIdx.x & 3; }
+
+// Load rows/cols [0, kb) of a column-major block, identity padding outside.
+__device__ __forceinline__ void blk_load(double (&a)[16], const double* __restrict__ g,
+                                         int64_t ld, int kb) {
+  const int c = blk_col(), part = blk_part();
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int i = part + 4 * q;
+    a[q] = (i < kb && c < kb) ? g[i + (int64_t)c * ld] : (i == c ? 1.0 : 0.0);
+  }
+}
+__device__ __forceinline__ void blk_store(const double (&a)[16], double* __restrict__ g, int64_t ld,
+                                          int kb) {
+  const int c = blk_col(), part = blk_part();
+  if (c >= kb) return;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int i = part + 4 * q;
+    if (i < kb) g[i + (int64_t)c * ld] = a[q];
+  }
+}
+__device__ __forceinline__ void blk_to_smem(const double (&a)[16], double (*S)[kBlk + 1]) {
+  const int c = blk_col(), part = blk_part();
+#pragma unroll
+  for (int q = 0; q < 16; ++q) S[part + 4 * q][c] = a[q];
+}
+
+// In-register factorisation of the 64 x 64 block (identity-padded beyond the
+// active size, so always 64 steps).  `line` needs 256 doubles of shared
+// memory.  *bad is set on a non-positive (CHOL) / zero (LU) pivot.
+//   CHOL: G = R^T R, a <- R (upper, strictly lower part zeroed)
+//   LU  : A = L U without pivoting, a <- L (unit, strictly lower) + U
+template <bool CHOL>
+__device__ __forceinline__ void blk_factor(double (&a)[16], double* line, int* bad) {
+  const int c = blk_col(), part = blk_part();
+#pragma unroll
+  for (int j = 0; j < kBlk; ++j) {
+    const int qj = j >> 2, pj = j & 3;
+    double* rb = line + (j & 1) * 128;  // pivot row
+    double* cb = rb + 64;               // pivot column (LU)
+    if (part == pj) rb[c] = a[qj];
+    if (!CHOL && c == j) {
+#pragma unroll
+      for (int q = qj; q < 16; ++q) cb[part + 4 * q] = a[q];
+    }
+    __syncthreads();
+    const double piv = rb[j];
+    if (CHOL) {
+      if (threadIdx.x == 0 && !(piv > 0.0)) *bad = 1;
+      const double inv = rsqrt(piv);
+      const double rc = rb[c] * inv;
+      if (part == pj) a[qj] = (c >= j) ? rc : 0.0;
+      if (c > j) {
+#pragma unroll
+        for (int q = qj; q < 16; ++q)
+          if (part + 4 * q > j) a[q] = fma(-rb[part + 4 * q] * inv, rc, a[q]);
+      }
+    } else {
+      if (threadIdx.x == 0 && !(fabs(piv) > 0.0)) *bad = 1;
+      const double inv = 1.0 / piv;
+      if (c == j) {
+#pragma unroll
+        for (int q = qj; q < 16; ++q)
+          if (part + 4 * q > j) a[q] *= inv;
+      } else if (c > j) {
+        const double uc = rb[c];
+#pragma unroll
+        for (int q = qj; q < 16; ++q)
+          if (part + 4 * q > j) a[q] = fma(-cb[part + 4 * q] * inv, uc, a[q]);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Inverses of the triangles of a factor held in shared memory S (64 x 64):
+// x <- U^{-1} (upper triangle incl. diagonal of S), and, if LOWER,
+// y <- L^{-1} (unit lower triangle of S).  Back / forward substitution on the
+// identity, right-looking, both sweeps sharing one barrier per step.
+// `line` needs 256 doubles, `dinv` 64 doubles of shared memory, both
+// scratch; S must be complete (barrier) on entry.
+template <bool LOWER>
+__device__ __forceinline__ void blk_tri_inverse(double (*S)[kBlk + 1], double (&x)[16],
+                                                double (&y)[16], double* line, double* dinv) {
+  const int c = blk_col(), part = blk_part();
+  if (threadIdx.x < kBlk) dinv[threadIdx.x] = 1.0 / S[threadIdx.x][threadIdx.x];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    x[q] = (part + 4 * q == c) ? 1.0 : 0.0;
+    if (LOWER) y[q] = x[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < kBlk; ++s) {
+    const int j = kBlk - 1 - s, qj = j >> 2, pj = j & 3;  // upper: rows bottom-up
+    const int k = s, qk = k >> 2, pk = k & 3;             // lower: rows top-down
+    double* ub = line + (s & 1) * 128;
+    double* lb = ub + 64;
+    if (part == pj) {
+      x[qj] *= dinv[j];
+      ub[c] = x[qj];
+    }
+    if (LOWER && part == pk) lb[c] = y[qk];
+    __syncthreads();
+    const double xj = ub[c];
+#pragma unroll
+    for (int q = 0; q <= qj; ++q)
+      if (part + 4 * q < j) x[q] = fma(-S[part + 4 * q][j], xj, x[q]);
+    if (LOWER) {
+      const double yk = lb[c];
+#pragma unroll
+      for (int q = qk; q < 16; ++q)
+        if (part + 4 * q > k) y[q] = fma(-S[part + 4 * q][k], yk, y[q]);
+    }
+  }
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------ GEMM

@@ -571,25 +571,23 @@ __global__ void __launch_bounds__(1024) sort_chop_kernel(int p, int k, const dou
 // ----------------------------------------------------------- certificate
 constexpr int TRB = 64;
 
-// Invert the 64x64 diagonal blocks of an upper-triangular R (one CTA each).
-__global__ void trinv_diag_kernel(int k, const double* __restrict__ R, int64_t ldr,
-                                  double* __restrict__ X, int64_t ldx) {
+// Invert the 64x64 diagonal blocks of an upper-triangular R (one CTA each),
+// block held in registers (common.cuh, blk_tri_inverse).
+__global__ void __launch_bounds__(256) trinv_diag_kernel(int k, const double* __restrict__ R,
+                                                         int64_t ldr, double* __restrict__ X,
+                                                         int64_t ldx) {
   extern __shared__ double tri_sm[];
-  double (*Rs)[TRB + 1] = reinterpret_cast<double (*)[TRB + 1]>(tri_sm);
-  double (*Xs)[TRB + 1] = reinterpret_cast<double (*)[TRB + 1]>(tri_sm + TRB * (TRB + 1));
+  double (*S)[kBlk + 1] = reinterpret_cast<double (*)[kBlk + 1]>(tri_sm);
+  double* line = tri_sm + kBlk * (kBlk + 1);
+  double* dinv = line + 256;
   const int b0 = blockIdx.x * TRB;
   const int nb = min(TRB, k - b0);
-  for (int idx = threadIdx.x; idx < TRB * TRB; idx += blockDim.x) {
-    const int r = idx % TRB, c = idx / TRB;
-    Rs[r][c] = (r < nb && c < nb) ? R[(b0 + r) + (int64_t)(b0 + c) * ldr] : (r == c ? 1.0 : 0.0);
-    Xs[r][c] = 0.0;
-  }
+  double a[16], x[16], y[16];
+  blk_load(a, R + b0 + (int64_t)b0 * ldr, ldr, nb);
+  blk_to_smem(a, S);
   __syncthreads();
-  upper_inverse_smem<TRB>(Rs, Xs, threadIdx.x);
-  for (int idx = threadIdx.x; idx < nb * nb; idx += blockDim.x) {
-    const int r = idx % nb, cc = idx / nb;
-    X[(b0 + r) + (int64_t)(b0 + cc) * ldx] = Xs[r][cc];
-  }
+  blk_tri_inverse<false>(S, x, y, line, dinv);
+  blk_store(x, X + b0 + (int64_t)b0 * ldx, ldx, nb);
 }
 
 // Deterministic two-stage sum of squares.
@@ -905,7 +903,7 @@ int tri_inverse(cudaStream_t s, int k, const double* R, int64_t ldr, double* X) 
   QTT_CUDA(cudaMallocAsync(&T, sizeof(double) * kk * kk, s));
   QTT_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * kk * kk, s));
   static bool configured = false;
-  const int tri_smem = (int)(2 * TRB * (TRB + 1) * sizeof(double));
+  const int tri_smem = (int)((kBlk * (kBlk + 1) + 256 + kBlk) * sizeof(double));
   if (!configured) {
     QTT_CUDA(cudaFuncSetAttribute(trinv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   tri_smem));

@@ -18,34 +18,28 @@ namespace qtt {
 namespace {
 
 constexpr int LB = 64;
-constexpr int kLuSmem = 2 * LB * (LB + 1) * sizeof(double);
+constexpr int kLuSmem = (kBlk * (kBlk + 1) + 256 + kBlk) * sizeof(double);
 
 // Factor the kb x kb diagonal block in place (L unit lower, U upper) and
-// write L^{-1} and U^{-1} (LB x LB, zero padded) to linv / uinv.
+// write L^{-1} and U^{-1} (LB x LB, identity padded) to linv / uinv.  The
+// block lives in registers (common.cuh, blk_factor / blk_tri_inverse).
 __global__ void __launch_bounds__(256) lu_diag_kernel(int kb, double* __restrict__ A, int64_t lda,
                                                       double* __restrict__ linv,
                                                       double* __restrict__ uinv,
                                                       int* __restrict__ bad) {
   extern __shared__ double lu_sm[];
-  double (*S)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(lu_sm);
-  double (*X)[LB + 1] = reinterpret_cast<double (*)[LB + 1]>(lu_sm + LB * (LB + 1));
-  const int tid = threadIdx.x;
-  for (int idx = tid; idx < LB * LB; idx += blockDim.x) {
-    const int r = idx % LB, c = idx / LB;
-    S[r][c] = (r < kb && c < kb) ? A[r + (int64_t)c * lda] : (r == c ? 1.0 : 0.0);
-  }
+  double (*S)[kBlk + 1] = reinterpret_cast<double (*)[kBlk + 1]>(lu_sm);
+  double* line = lu_sm + kBlk * (kBlk + 1);
+  double* dinv = line + 256;
+  double a[16], x[16], y[16];
+  blk_load(a, A, lda, kb);
+  blk_factor<false>(a, line, bad);
+  blk_store(a, A, lda, kb);
+  blk_to_smem(a, S);
   __syncthreads();
-  crout_factor64<false>(S, &X[0][0], kb, bad);
-  for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
-    const int r = idx % kb, c = idx / kb;
-    A[r + (int64_t)c * lda] = S[r][c];
-  }
-  __syncthreads();
-  upper_inverse_smem<LB>(S, X, tid);
-  for (int idx = tid; idx < LB * LB; idx += blockDim.x) uinv[idx] = X[idx % LB][idx / LB];
-  __syncthreads();
-  unit_lower_inverse_smem<LB>(S, X, tid);
-  for (int idx = tid; idx < LB * LB; idx += blockDim.x) linv[idx] = X[idx % LB][idx / LB];
+  blk_tri_inverse<true>(S, x, y, line, dinv);
+  blk_store(x, uinv, LB, LB);
+  blk_store(y, linv, LB, LB);
 }
 
 __global__ void residual_norms_kernel(int n, const double* __restrict__ r,
