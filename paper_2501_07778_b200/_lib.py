@@ -13,7 +13,9 @@ import os
 import torch
 
 MAX_CORES = 64
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libqttb200.so")
+_LIB_PATH = os.environ.get(
+    "QTT_LIB_PATH",  # A/B builds of the same library (tools/)
+    os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libqttb200.so"))
 
 QTT_OK, QTT_EINVAL, QTT_ECUDA, QTT_EWORKSPACE, QTT_EUNSUPPORTED = range(5)
 

@@ -58,11 +58,12 @@ __global__ void __launch_bounds__(256) chol_panel_kernel(int kb, const double* _
   for (int j = 0; j < kBlk; ++j) {
     const int qj = j >> 2, pj = j & 3;
     const double v = x[qj] * dinv[j];
-    const double xj = __shfl_sync(0xffffffffu, v, (lane & ~3) | pj);
+    const double xj = -__shfl_sync(0xffffffffu, v, (lane & ~3) | pj);
+    const double* r = &S[j][part];
     if (part == pj) x[qj] = v;
+    if (part > pj) x[qj] = fma(r[4 * qj], xj, x[qj]);
 #pragma unroll
-    for (int q = qj; q < 16; ++q)
-      if (part + 4 * q > j) x[q] = fma(-S[j][part + 4 * q], xj, x[q]);
+    for (int q = qj + 1; q < 16; ++q) x[q] = fma(r[4 * q], xj, x[q]);
   }
   if (act) {
 #pragma unroll
@@ -73,15 +74,23 @@ __global__ void __launch_bounds__(256) chol_panel_kernel(int kb, const double* _
   }
 }
 
-// G(diag block b) <- rblk[b] (upper incl. diagonal; strictly lower zero).
+// G(diag block b) <- rblk[b] (upper incl. diagonal; strictly lower zero) and
+// zero block column b below its diagonal block.
 __global__ void __launch_bounds__(256) chol_diag_writeback_kernel(int n, const double* __restrict__ rblk,
                                                                   double* __restrict__ G, int64_t ldg) {
   const int b0 = blockIdx.x * kBlk;
   const int kb = min(kBlk, n - b0);
   const double* src = rblk + (int64_t)blockIdx.x * kBlk * kBlk;
-  for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
-    const int r = idx % kb, c = idx / kb;
-    G[(b0 + r) + (int64_t)(b0 + c) * ldg] = src[r + c * kBlk];
+  if (blockIdx.y == 0)
+    for (int idx = threadIdx.x; idx < kb * kb; idx += blockDim.x) {
+      const int r = idx % kb, c = idx / kb;
+      G[(b0 + r) + (int64_t)(b0 + c) * ldg] = src[r + c * kBlk];
+    }
+  const int below = n - b0 - kb;
+  for (int64_t idx = blockIdx.y * blockDim.x + threadIdx.x; idx < (int64_t)below * kb;
+       idx += (int64_t)gridDim.y * blockDim.x) {
+    const int r = (int)(idx % below), c = (int)(idx / below);
+    G[(b0 + kb + r) + (int64_t)(b0 + c) * ldg] = 0.0;
   }
 }
 
@@ -93,8 +102,9 @@ __global__ void gram_defect_kernel(int n, const double* __restrict__ G, int64_t 
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)n * n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(i % n), c = (int)(i / n);
+    if (r > c) continue;  // G holds its upper triangle only
     const double v = G[r + (int64_t)c * ldg] - (r == c ? 1.0 : 0.0);
-    a = fma(v, v, a);
+    a = fma(r == c ? v : 2.0 * v, v, a);
   }
   a = warp_sum(a);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
@@ -127,14 +137,11 @@ int chol_upper(cudaStream_t s, int n, double* G, int64_t ldg, double* rblk, int*
         kb, Gkk, ldg, rblk + (int64_t)nblk * CB * CB, G12, rest, bad);
     QTT_CHECK_LAUNCH();
     if (rest <= 0) continue;
-    // G22 -= R12^T R12 (full square update; only the upper part is used)
+    // G22 -= R12^T R12 (upper tiles only)
     double* G22 = G + (k0 + kb) + (int64_t)(k0 + kb) * ldg;
-    QTT_TRY(dgemm(s, 1, 0, rest, rest, kb, -1.0, G12, ldg, G12, ldg, 1.0, G22, ldg));
-    // zero the strictly lower block column below the diagonal block
-    QTT_CUDA(cudaMemset2DAsync(G + (k0 + kb) + (int64_t)k0 * ldg, sizeof(double) * ldg, 0,
-                               sizeof(double) * rest, kb, s));
+    QTT_TRY(dgemm(s, 1, 0, rest, rest, kb, -1.0, G12, ldg, G12, ldg, 1.0, G22, ldg, kGemmUpperC));
   }
-  chol_diag_writeback_kernel<<<nblk, 256, 0, s>>>(n, rblk, G, ldg);
+  chol_diag_writeback_kernel<<<dim3(nblk, 16), 256, 0, s>>>(n, rblk, G, ldg);
   QTT_CHECK_LAUNCH();
   return kOk;
 }
@@ -160,7 +167,7 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
   int status = kOk;
   do {
     // pass 1: G = A^T A = R1^T R1, Q1 = A R1^{-1}
-    if ((status = dgemm(s, 1, 0, n, n, m, 1.0, A, lda, A, lda, 0.0, G, nn)) != kOk) break;
+    if ((status = dgemm(s, 1, 0, n, n, m, 1.0, A, lda, A, lda, 0.0, G, nn, kGemmUpperC)) != kOk) break;
     if ((status = chol_upper(s, n, G, nn, rblk, bad)) != kOk) break;
     int hbad = 0;
     QTT_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -168,9 +175,9 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
     if (hbad) break;
     QTT_CUDA(cudaMemcpyAsync(R1, G, sizeof(double) * nn * nn, cudaMemcpyDeviceToDevice, s));
     if ((status = tri_inverse(s, n, R1, nn, Ri)) != kOk) break;
-    if ((status = dgemm(s, 0, 0, m, n, n, 1.0, A, lda, Ri, nn, 0.0, Q1, m)) != kOk) break;
+    if ((status = dgemm(s, 0, 0, m, n, n, 1.0, A, lda, Ri, nn, 0.0, Q1, m, kGemmTriB)) != kOk) break;
     // pass 2: certify cond(Q1) ~ 1, then G = Q1^T Q1 = R2^T R2, Q = Q1 R2^{-1}
-    if ((status = dgemm(s, 1, 0, n, n, m, 1.0, Q1, m, Q1, m, 0.0, G, nn)) != kOk) break;
+    if ((status = dgemm(s, 1, 0, n, n, m, 1.0, Q1, m, Q1, m, 0.0, G, nn, kGemmUpperC)) != kOk) break;
     gram_defect_kernel<<<kDefectParts, 256, 0, s>>>(n, G, nn, parts);
     QTT_CHECK_LAUNCH();
     sum_parts_kernel<<<1, 32, 0, s>>>(kDefectParts, parts, scal);
@@ -185,9 +192,9 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
     QTT_CUDA(cudaStreamSynchronize(s));
     if (hbad) break;
     if ((status = tri_inverse(s, n, G, nn, Ri)) != kOk) break;
-    if ((status = dgemm(s, 0, 0, m, n, n, 1.0, Q1, m, Ri, nn, 0.0, Q, ldq)) != kOk) break;
+    if ((status = dgemm(s, 0, 0, m, n, n, 1.0, Q1, m, Ri, nn, 0.0, Q, ldq, kGemmTriB)) != kOk) break;
     // R = R2 R1 (product of upper-triangular factors stays upper triangular)
-    if ((status = dgemm(s, 0, 0, n, n, n, 1.0, G, nn, R1, nn, 0.0, R, ldr)) != kOk) break;
+    if ((status = dgemm(s, 0, 0, n, n, n, 1.0, G, nn, R1, nn, 0.0, R, ldr, kGemmTriA | kGemmTriB)) != kOk) break;
     *ok = 1;
   } while (false);
   QTT_CUDA(cudaFreeAsync(G, s));

@@ -127,28 +127,33 @@ __device__ __forceinline__ void blk_factor(double (&a)[16], double* line, int* b
     }
     __syncthreads();
     const double piv = rb[j];
+    // Row i = part + 4q lies below the pivot iff q > qj, or q == qj and
+    // part > pj: only the q == qj entry needs a predicate.
     if (CHOL) {
       if (threadIdx.x == 0 && !(piv > 0.0)) *bad = 1;
       const double inv = rsqrt(piv);
       const double rc = rb[c] * inv;
       if (part == pj) a[qj] = (c >= j) ? rc : 0.0;
       if (c > j) {
+        const double t = -rc * inv;  // G[i][c] -= (G[j][i] / sqrt(piv)) * R[j][c]
+        const double* r = rb + part;
+        if (part > pj) a[qj] = fma(r[4 * qj], t, a[qj]);
 #pragma unroll
-        for (int q = qj; q < 16; ++q)
-          if (part + 4 * q > j) a[q] = fma(-rb[part + 4 * q] * inv, rc, a[q]);
+        for (int q = qj + 1; q < 16; ++q) a[q] = fma(r[4 * q], t, a[q]);
       }
     } else {
       if (threadIdx.x == 0 && !(fabs(piv) > 0.0)) *bad = 1;
       const double inv = 1.0 / piv;
       if (c == j) {
+        if (part > pj) a[qj] *= inv;
 #pragma unroll
-        for (int q = qj; q < 16; ++q)
-          if (part + 4 * q > j) a[q] *= inv;
+        for (int q = qj + 1; q < 16; ++q) a[q] *= inv;
       } else if (c > j) {
-        const double uc = rb[c];
+        const double t = -rb[c] * inv;  // A[i][c] -= (A[i][j] / piv) * U[j][c]
+        const double* l = cb + part;
+        if (part > pj) a[qj] = fma(l[4 * qj], t, a[qj]);
 #pragma unroll
-        for (int q = qj; q < 16; ++q)
-          if (part + 4 * q > j) a[q] = fma(-cb[part + 4 * q] * inv, uc, a[q]);
+        for (int q = qj + 1; q < 16; ++q) a[q] = fma(l[4 * q], t, a[q]);
       }
     }
   }
@@ -184,15 +189,15 @@ __device__ __forceinline__ void blk_tri_inverse(double (*S)[kBlk + 1], double (&
     }
     if (LOWER && part == pk) lb[c] = y[qk];
     __syncthreads();
-    const double xj = ub[c];
+    const double xj = -ub[c];
 #pragma unroll
-    for (int q = 0; q <= qj; ++q)
-      if (part + 4 * q < j) x[q] = fma(-S[part + 4 * q][j], xj, x[q]);
+    for (int q = 0; q < qj; ++q) x[q] = fma(S[part + 4 * q][j], xj, x[q]);
+    if (part < pj) x[qj] = fma(S[part + 4 * qj][j], xj, x[qj]);
     if (LOWER) {
-      const double yk = lb[c];
+      const double yk = -lb[c];
+      if (part > pk) y[qk] = fma(S[part + 4 * qk][k], yk, y[qk]);
 #pragma unroll
-      for (int q = qk; q < 16; ++q)
-        if (part + 4 * q > k) y[q] = fma(-S[part + 4 * q][k], yk, y[q]);
+      for (int q = qk + 1; q < 16; ++q) y[q] = fma(S[part + 4 * q][k], yk, y[q]);
     }
   }
   __syncthreads();
@@ -213,7 +218,12 @@ struct GemmArgs {
   double* c;
   int64_t ldc, stride_c;
   int batch;
+  int flags = 0;  // kGemm* structure flags below
 };
+// Structure flags (tiles of 64): only the upper-triangular tiles of C are
+// computed (the strictly lower tiles of C are left unspecified); op(A) / op(B)
+// are upper triangular, so each tile's K range is clipped to the nonzeros.
+constexpr int kGemmUpperC = 1, kGemmTriA = 2, kGemmTriB = 4;
 
 int gemm(const GemmArgs& g, cudaStream_t stream);
 
@@ -236,8 +246,8 @@ GemmProfile& gemm_profile();
 // Convenience: single column-major GEMM.
 inline int dgemm(cudaStream_t s, int ta, int tb, int m, int n, int k, double alpha,
                  const double* a, int64_t lda, const double* b, int64_t ldb,
-                 double beta, double* c, int64_t ldc) {
-  GemmArgs g{m, n, k, ta, tb, alpha, beta, a, lda, 0, b, ldb, 0, c, ldc, 0, 1};
+                 double beta, double* c, int64_t ldc, int flags = 0) {
+  GemmArgs g{m, n, k, ta, tb, alpha, beta, a, lda, 0, b, ldb, 0, c, ldc, 0, 1, flags};
   return gemm(g, s);
 }
 

@@ -12,7 +12,11 @@
 namespace qtt {
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, PAD = 4, THREADS = 128;
+#ifndef QTT_GEMM_STAGES
+#define QTT_GEMM_STAGES 4
+#endif
+constexpr int BM = 64, BN = 64, BK = 16, PAD = 4, THREADS = 128, STAGES = QTT_GEMM_STAGES;
+constexpr int kGemmSmem = STAGES * BK * (BM + PAD + BN + PAD) * sizeof(double);
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -32,8 +36,9 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 template <int TA, int TB>
 __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int kchunk, double* ws) {
-  __shared__ double As[2][BK][BM + PAD];
-  __shared__ double Bs[2][BK][BN + PAD];
+  extern __shared__ double gemm_sm[];
+  double (*As)[BK][BM + PAD] = reinterpret_cast<double (*)[BK][BM + PAD]>(gemm_sm);
+  double (*Bs)[BK][BN + PAD] = reinterpret_cast<double (*)[BK][BN + PAD]>(gemm_sm + STAGES * BK * (BM + PAD));
 
   const int tile = blockIdx.x;
   const int m0 = (tile % mt) * BM;
@@ -43,8 +48,16 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int k
   const double* B = g.b + bz * g.stride_b;
   double* C = g.c + bz * g.stride_c;
   const int M = g.m, N = g.n;
-  const int kbeg = blockIdx.z * kchunk;
-  const int K = min(g.k, kbeg + kchunk);  // tiles cover [kbeg, K)
+  int kbeg = blockIdx.z * kchunk;
+  int K = min(g.k, kbeg + kchunk);  // tiles cover [kbeg, K)
+  if (g.flags) {
+    if ((g.flags & kGemmUpperC) && m0 > n0) {
+      if (ws == nullptr) return;
+      K = kbeg;  // split-K partial of a skipped tile: zeros
+    }
+    if (g.flags & kGemmTriA) kbeg = max(kbeg, m0);
+    if (g.flags & kGemmTriB) K = min(K, n0 + BN);
+  }
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
 
@@ -69,7 +82,6 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int k
       const double* src = ok ? (TB == 0 ? B + gk + (int64_t)gn * g.ldb : B + gn + (int64_t)gk * g.ldb) : B;
       cp_async8(&Bs[buf][kk][nn], src, ok);
     }
-    cp_async_commit();
   };
 
   double acc[4][4][2];
@@ -79,16 +91,21 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int k
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int ktiles = (K - kbeg + BK - 1) / BK;
-  if (ktiles > 0) load_tile(0, kbeg);
+  // STAGES-deep cp.async pipeline: tiles kt+1 .. kt+STAGES-1 are in flight
+  // while tile kt is multiplied (one commit group per tile, empty groups at
+  // the tail keep the wait count uniform).
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < ktiles) load_tile(st, kbeg + st * BK);
+    cp_async_commit();
+  }
   for (int kt = 0; kt < ktiles; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < ktiles) {
-      load_tile(buf ^ 1, kbeg + (kt + 1) * BK);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();  // tile kt landed for all threads; buffer (kt-1) % STAGES is free
+    const int nxt = kt + STAGES - 1;
+    if (nxt < ktiles) load_tile(nxt % STAGES, kbeg + nxt * BK);
+    cp_async_commit();
+    const int buf = kt % STAGES;
 #pragma unroll
     for (int ks = 0; ks < BK; ks += 4) {
       double af[4], bf[4];
@@ -102,8 +119,8 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int k
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
 
   if (ws != nullptr) {
     // split-K partial: plain accumulator into ws[(z * batch + b) * M * N]
@@ -123,6 +140,34 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int k
     return;
   }
   const double alpha = g.alpha, beta = g.beta;
+  if (beta != 0.0) {
+    // all C loads in flight before the first store (no load-store chain)
+    double cv[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = m0 + wm + i * 8 + (lane >> 2);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = n0 + wn + j * 8 + 2 * (lane & 3) + h;
+          cv[i][j][h] = (row < M && col < N) ? __ldg(C + row + (int64_t)col * g.ldc) : 0.0;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) acc[i][j][h] = fma(alpha, acc[i][j][h], beta * cv[i][j][h]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) acc[i][j][h] *= alpha;
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int row = m0 + wm + i * 8 + (lane >> 2);
@@ -132,12 +177,7 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int k
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int col = n0 + wn + j * 8 + 2 * (lane & 3) + h;
-        if (col < N) {
-          double* p = C + row + (int64_t)col * g.ldc;
-          double v = alpha * acc[i][j][h];
-          if (beta != 0.0) v += beta * *p;
-          *p = v;
-        }
+        if (col < N) C[row + (int64_t)col * g.ldc] = acc[i][j][h];
       }
     }
   }
@@ -260,10 +300,18 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
   if (splits > 1)
     QTT_CUDA(cudaMallocAsync(&ws, sizeof(double) * splits * g.batch * (int64_t)g.m * g.n, stream));
   grid.z = splits;
-  if (!g.trans_a && !g.trans_b) gemm_kernel<0, 0><<<grid, THREADS, 0, stream>>>(g, mt, kchunk, ws);
-  else if (!g.trans_a && g.trans_b) gemm_kernel<0, 1><<<grid, THREADS, 0, stream>>>(g, mt, kchunk, ws);
-  else if (g.trans_a && !g.trans_b) gemm_kernel<1, 0><<<grid, THREADS, 0, stream>>>(g, mt, kchunk, ws);
-  else gemm_kernel<1, 1><<<grid, THREADS, 0, stream>>>(g, mt, kchunk, ws);
+  static bool configured = false;
+  if (!configured) {
+    QTT_CUDA(cudaFuncSetAttribute(gemm_kernel<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem));
+    QTT_CUDA(cudaFuncSetAttribute(gemm_kernel<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem));
+    QTT_CUDA(cudaFuncSetAttribute(gemm_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem));
+    QTT_CUDA(cudaFuncSetAttribute(gemm_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem));
+    configured = true;
+  }
+  if (!g.trans_a && !g.trans_b) gemm_kernel<0, 0><<<grid, THREADS, kGemmSmem, stream>>>(g, mt, kchunk, ws);
+  else if (!g.trans_a && g.trans_b) gemm_kernel<0, 1><<<grid, THREADS, kGemmSmem, stream>>>(g, mt, kchunk, ws);
+  else if (g.trans_a && !g.trans_b) gemm_kernel<1, 0><<<grid, THREADS, kGemmSmem, stream>>>(g, mt, kchunk, ws);
+  else gemm_kernel<1, 1><<<grid, THREADS, kGemmSmem, stream>>>(g, mt, kchunk, ws);
   QTT_CHECK_LAUNCH();
   if (splits > 1) {
     const int64_t total = (int64_t)g.m * g.n * g.batch;
@@ -275,7 +323,19 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
   if (prof.on) {
     QTT_CUDA(cudaEventRecord(e1, stream));
     prof.events.emplace_back(e0, e1);
-    const double f = 2.0 * g.m * (double)g.n * g.k * g.batch;
+    double f = 2.0 * g.m * (double)g.n * g.k * g.batch;
+    if (g.flags) {  // multiply-adds of the tiles actually computed
+      f = 0.0;
+      for (int mi = 0; mi < mt; ++mi)
+        for (int64_t ni = 0; ni < tiles / mt; ++ni) {
+          if ((g.flags & kGemmUpperC) && mi > ni) continue;
+          const int64_t klo = (g.flags & kGemmTriA) ? (int64_t)mi * BM : 0;
+          const int64_t khi = (g.flags & kGemmTriB) ? std::min<int64_t>(g.k, (ni + 1) * BN) : g.k;
+          if (khi > klo)
+            f += 2.0 * std::min(BM, g.m - mi * BM) * std::min<int64_t>(BN, g.n - ni * BN) * (khi - klo);
+        }
+      f *= g.batch;
+    }
     prof.launch_flops.push_back(f);
     prof.flops += f;
   }
