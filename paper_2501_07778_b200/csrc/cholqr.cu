@@ -124,6 +124,59 @@ __global__ void sum_parts_kernel(int n, const double* __restrict__ part, double*
   }
 }
 
+// U <- split(G - I - W): strictly upper part of (G - I - W) plus half its
+// diagonal (upper triangle of U, lower zeroed).  W may be null (W = 0).
+__global__ void near_identity_split_kernel(int n, const double* __restrict__ G, int64_t ldg,
+                                           const double* __restrict__ W, int64_t ldw,
+                                           double* __restrict__ U, int64_t ldu) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx % n), c = (int)(idx / n);
+    double v = 0.0;
+    if (r <= c) {
+      v = G[r + (int64_t)c * ldg] - (r == c ? 1.0 : 0.0);
+      if (W) v -= W[r + (int64_t)c * ldw];
+      if (r == c) v *= 0.5;
+    }
+    U[r + (int64_t)c * ldu] = v;
+  }
+}
+
+// G <- I + U (upper), in place.
+__global__ void add_identity_kernel(int n, const double* __restrict__ U, int64_t ldu,
+                                    double* __restrict__ G, int64_t ldg) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx % n), c = (int)(idx / n);
+    G[r + (int64_t)c * ldg] = U[r + (int64_t)c * ldu] + (r == c ? 1.0 : 0.0);
+  }
+}
+
+// Cholesky factor of a Gram matrix close to the identity, G = I + E with
+// ||E||_F = delta small (the second CholeskyQR pass), without the
+// sequential factorisation: R = I + U with U upper triangular solving
+// U + U^T = E - U^T U, by the fixed-point iteration
+//   U_0 = split(E),  U_{k+1} = split(E - U_k^T U_k),
+// split = strict upper part + half the diagonal.  The error contracts as
+// delta^(k+2), so `iters` = smallest k with delta^(k+2) <= 1e-17; each
+// iteration is one triangular DMMA GEMM (lower x upper, upper tiles only).
+int chol_near_identity(cudaStream_t s, int n, double* G, int64_t ldg, double* U, double* W,
+                       int iters) {
+  const int64_t nn = n;
+  const int blocks = (int)std::min<int64_t>(ceil_div(nn * nn, 256), 8 * num_sms());
+  near_identity_split_kernel<<<blocks, 256, 0, s>>>(n, G, ldg, nullptr, 0, U, nn);
+  QTT_CHECK_LAUNCH();
+  for (int it = 0; it < iters; ++it) {
+    QTT_TRY(dgemm(s, 1, 0, n, n, n, 1.0, U, nn, U, nn, 0.0, W, nn,
+                  kGemmUpperC | kGemmLowA | kGemmTriB));
+    near_identity_split_kernel<<<blocks, 256, 0, s>>>(n, G, ldg, W, nn, U, nn);
+    QTT_CHECK_LAUNCH();
+  }
+  add_identity_kernel<<<blocks, 256, 0, s>>>(n, U, nn, G, ldg);
+  QTT_CHECK_LAUNCH();
+  return kOk;
+}
+
 // Blocked right-looking upper Cholesky G = R^T R (in place).  rblk: scratch
 // for the ceil(n/64) diagonal factors (64 x 64 each).
 int chol_upper(cudaStream_t s, int n, double* G, int64_t ldg, double* rblk, int* bad) {
@@ -186,11 +239,24 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
     QTT_CUDA(cudaMemcpyAsync(&defect, scal, sizeof(double), cudaMemcpyDeviceToHost, s));
     QTT_CUDA(cudaStreamSynchronize(s));
     if (getenv("QTT_QR_DEBUG")) fprintf(stderr, "[cholqr2] m=%d n=%d defect=%.3e\n", m, n, std::sqrt(defect));
-    if (!(std::sqrt(defect) <= 0.25)) break;
-    if ((status = chol_upper(s, n, G, nn, rblk, bad)) != kOk) break;
-    QTT_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-    QTT_CUDA(cudaStreamSynchronize(s));
-    if (hbad) break;
+    const double delta = std::sqrt(defect);
+    if (!(delta <= 0.25)) break;
+    if (delta <= 1e-2 && !getenv("QTT_NO_NEAR_IDENTITY")) {
+      int iters = 0;
+      while (iters < 8 && std::pow(std::max(delta, 1e-300), iters + 2) > 1e-17) ++iters;
+      double *U, *W;
+      QTT_CUDA(cudaMallocAsync(&U, sizeof(double) * nn * nn, s));
+      QTT_CUDA(cudaMallocAsync(&W, sizeof(double) * nn * nn, s));
+      status = chol_near_identity(s, n, G, nn, U, W, iters);
+      QTT_CUDA(cudaFreeAsync(U, s));
+      QTT_CUDA(cudaFreeAsync(W, s));
+      if (status != kOk) break;
+    } else {
+      if ((status = chol_upper(s, n, G, nn, rblk, bad)) != kOk) break;
+      QTT_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+      QTT_CUDA(cudaStreamSynchronize(s));
+      if (hbad) break;
+    }
     if ((status = tri_inverse(s, n, G, nn, Ri)) != kOk) break;
     if ((status = dgemm(s, 0, 0, m, n, n, 1.0, Q1, m, Ri, nn, 0.0, Q, ldq, kGemmTriB)) != kOk) break;
     // R = R2 R1 (product of upper-triangular factors stays upper triangular)

@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int k
     }
     if (g.flags & kGemmTriA) kbeg = max(kbeg, m0);
     if (g.flags & kGemmTriB) K = min(K, n0 + BN);
+    if (g.flags & kGemmLowA) K = min(K, m0 + BM);
   }
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
@@ -330,7 +331,8 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
         for (int64_t ni = 0; ni < tiles / mt; ++ni) {
           if ((g.flags & kGemmUpperC) && mi > ni) continue;
           const int64_t klo = (g.flags & kGemmTriA) ? (int64_t)mi * BM : 0;
-          const int64_t khi = (g.flags & kGemmTriB) ? std::min<int64_t>(g.k, (ni + 1) * BN) : g.k;
+          int64_t khi = (g.flags & kGemmTriB) ? std::min<int64_t>(g.k, (ni + 1) * BN) : g.k;
+          if (g.flags & kGemmLowA) khi = std::min<int64_t>(khi, (int64_t)(mi + 1) * BM);
           if (khi > klo)
             f += 2.0 * std::min(BM, g.m - mi * BM) * std::min<int64_t>(BN, g.n - ni * BN) * (khi - klo);
         }

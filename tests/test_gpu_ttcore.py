@@ -249,7 +249,7 @@ def test_qr_very_tall_uses_16_wide_panels():
     assert np.abs(q.T @ q - np.eye(n)).max() < 1e-12
 
 
-@pytest.mark.parametrize("cond", [1e2, 1e6, 1e12])
+@pytest.mark.parametrize("cond", [1e0, 1e2, 1e3, 1e4, 1e5, 1e6, 1e12])
 def test_qr_cholqr_path_and_fallback(cond):
     """n >= 128 tries CholeskyQR2; ill-conditioned inputs fall back to
     Householder.  Both must give an orthonormal Q and A = QR."""
