@@ -179,20 +179,53 @@ int chol_near_identity(cudaStream_t s, int n, double* G, int64_t ldg, double* U,
 
 // Blocked right-looking upper Cholesky G = R^T R (in place).  rblk: scratch
 // for the ceil(n/64) diagonal factors (64 x 64 each).
+//
+// Look-ahead of depth one: the critical path (panel k = factor + block-row
+// solve, then the update of block row k+1 only, "a_k") runs on the
+// high-priority side stream, while the rest of the trailing update ("b_k",
+// rows/cols beyond block k+1, upper tiles) runs on `s` concurrently with
+// panel k+1.  Dependencies: a_k after b_{k-1} (both update block row k+1),
+// b_k after panel k; disjoint writes otherwise.
 int chol_upper(cudaStream_t s, int n, double* G, int64_t ldg, double* rblk, int* bad) {
+  static cudaEvent_t ev[6] = {};
+  if (!ev[0])
+    for (auto& e : ev) QTT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  cudaEvent_t *evP = ev, *evB = ev + 2, evStart = ev[4], evEnd = ev[5];
+  cudaStream_t ss = side_stream();
+  const bool ahead = ss != s && !getenv("QTT_NO_LOOKAHEAD");
+  cudaStream_t sp = ahead ? ss : s;  // critical-path stream
+  if (ahead) {
+    QTT_CUDA(cudaEventRecord(evStart, s));
+    QTT_CUDA(cudaStreamWaitEvent(ss, evStart, 0));
+  }
   int nblk = 0;
   for (int k0 = 0; k0 < n; k0 += CB, ++nblk) {
+    const int k = nblk;
     const int kb = std::min(CB, n - k0);
     const int rest = n - k0 - kb;
     const double* Gkk = G + k0 + (int64_t)k0 * ldg;
     double* G12 = G + k0 + (int64_t)(k0 + kb) * ldg;
-    chol_panel_kernel<<<std::max(1, (int)ceil_div(rest, CB)), 256, 0, s>>>(
-        kb, Gkk, ldg, rblk + (int64_t)nblk * CB * CB, G12, rest, bad);
+    chol_panel_kernel<<<std::max(1, (int)ceil_div(rest, CB)), 256, 0, sp>>>(
+        kb, Gkk, ldg, rblk + (int64_t)k * CB * CB, G12, rest, bad);
     QTT_CHECK_LAUNCH();
     if (rest <= 0) continue;
-    // G22 -= R12^T R12 (upper tiles only)
+    const int kb1 = std::min(CB, rest), rest2 = rest - kb1;
     double* G22 = G + (k0 + kb) + (int64_t)(k0 + kb) * ldg;
-    QTT_TRY(dgemm(s, 1, 0, rest, rest, kb, -1.0, G12, ldg, G12, ldg, 1.0, G22, ldg, kGemmUpperC));
+    if (ahead) QTT_CUDA(cudaEventRecord(evP[k & 1], ss));
+    // a_k: block row k+1 -= R12[:, :kb1]^T R12
+    if (ahead && k > 0) QTT_CUDA(cudaStreamWaitEvent(ss, evB[(k - 1) & 1], 0));
+    QTT_TRY(dgemm(sp, 1, 0, kb1, rest, kb, -1.0, G12, ldg, G12, ldg, 1.0, G22, ldg));
+    if (rest2 <= 0) continue;
+    // b_k: the rest of G22 (upper tiles)
+    if (ahead) QTT_CUDA(cudaStreamWaitEvent(s, evP[k & 1], 0));
+    const double* R12b = G12 + (int64_t)kb1 * ldg;
+    QTT_TRY(dgemm(s, 1, 0, rest2, rest2, kb, -1.0, R12b, ldg, R12b, ldg, 1.0,
+                  G22 + kb1 + (int64_t)kb1 * ldg, ldg, kGemmUpperC));
+    if (ahead) QTT_CUDA(cudaEventRecord(evB[k & 1], s));
+  }
+  if (ahead) {
+    QTT_CUDA(cudaEventRecord(evEnd, ss));
+    QTT_CUDA(cudaStreamWaitEvent(s, evEnd, 0));
   }
   chol_diag_writeback_kernel<<<dim3(nblk, 16), 256, 0, s>>>(n, rblk, G, ldg);
   QTT_CHECK_LAUNCH();

@@ -46,6 +46,10 @@ int fetch(cudaStream_t s, const T* dev, T* host) {
 }
 
 // Right-to-left orthogonalisation of merged order-3 cores held in slots.
+// A core whose right unfolding is wide (n_k r_{k+1} < r_k) needs no QR: the
+// unfolding itself is the carry and the core becomes the identity, which is
+// right-orthonormal; the bond rank drops to its structural bound n_k r_{k+1}
+// exactly as the reference's QR would drop it (ttcore.py:296-306).
 int qr_sweep_right(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vector<int64_t>& n,
                    const std::vector<int64_t>& off, double* work, double* tq, double* tr,
                    double* tc) {
@@ -53,16 +57,51 @@ int qr_sweep_right(cudaStream_t s, int d, std::vector<int64_t>& r, const std::ve
     const int rows = (int)(n[k] * r[k + 1]);
     const int cols = (int)r[k];
     const int kk = std::min(rows, cols);
-    QTT_TRY(qr(s, rows, cols, work + off[k], rows, tq, rows, tr, kk));
-    QTT_CUDA(cudaMemcpyAsync(work + off[k], tq, sizeof(double) * rows * (int64_t)kk,
-                             cudaMemcpyDeviceToDevice, s));
     const int prev = (int)(r[k - 1] * n[k - 1]);
-    QTT_TRY(dgemm(s, 0, 0, kk, prev, cols, 1.0, tr, kk, work + off[k - 1], cols, 0.0, tc, kk));
+    if (rows < cols) {
+      // M = I * M: prev_new (rows x prev) = M (rows x cols) * prev (cols x prev)
+      QTT_TRY(dgemm(s, 0, 0, rows, prev, cols, 1.0, work + off[k], rows, work + off[k - 1], cols,
+                    0.0, tc, rows));
+      QTT_TRY(set_identity(s, rows, rows, work + off[k], rows));
+    } else {
+      QTT_TRY(qr(s, rows, cols, work + off[k], rows, tq, rows, tr, kk));
+      QTT_CUDA(cudaMemcpyAsync(work + off[k], tq, sizeof(double) * rows * (int64_t)kk,
+                               cudaMemcpyDeviceToDevice, s));
+      QTT_TRY(dgemm(s, 0, 0, kk, prev, cols, 1.0, tr, kk, work + off[k - 1], cols, 0.0, tc, kk));
+    }
     QTT_CUDA(cudaMemcpyAsync(work + off[k - 1], tc, sizeof(double) * kk * (int64_t)prev,
                              cudaMemcpyDeviceToDevice, s));
     r[k] = kk;
   }
   return kOk;
+}
+
+// Left structural reduction: while the left unfolding of core k is wide
+// (r_k n_k < r_{k+1}), multiply it into core k+1 and make core k the
+// identity.  Exact (no truncation decision; every bond is still examined by
+// the truncation sweep), and it removes the full-rank Householder/Cholesky
+// QRs the right-to-left sweep would otherwise spend on cores whose bond
+// ranks exceed the structural bound prod_{i<=k} n_i.
+void reduce_left(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vector<int64_t>& n,
+                 const std::vector<int64_t>& off, double* work, double* tc, int* status) {
+  *status = kOk;
+  for (int k = 0; k < d - 1; ++k) {
+    const int m = (int)(r[k] * n[k]);
+    const int N = (int)r[k + 1];
+    if (m >= N) break;
+    const int mc = (int)(n[k + 1] * r[k + 2]);
+    double* core = work + off[k];
+    double* next = work + off[k + 1];
+    // next_new (col-major mc x m) = next (mc x N) * L^T (N x m; L^T col-major == core)
+    if ((*status = dgemm(s, 0, 0, mc, m, N, 1.0, next, mc, core, N, 0.0, tc, mc)) != kOk) return;
+    if ((*status = set_identity(s, m, m, core, m)) != kOk) return;
+    if (cudaMemcpyAsync(next, tc, sizeof(double) * (int64_t)mc * m, cudaMemcpyDeviceToDevice, s) !=
+        cudaSuccess) {
+      *status = kCuda;
+      return;
+    }
+    r[k + 1] = m;
+  }
 }
 
 }  // namespace
@@ -88,6 +127,9 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
   int* perm = reinterpret_cast<int*>(sc.p + 8 + maxcore);
   int* flags = reinterpret_cast<int*>(sc.p + 2);  // [0]: cert ok, [1]: rank
 
+  int st = kOk;
+  reduce_left(s, d, r, n, off, work, tc.p, &st);
+  QTT_TRY(st);
   QTT_TRY(qr_sweep_right(s, d, r, n, off, work, tq.p, tr.p, tc.p));
   QTT_TRY(frob_norm(s, r[0] * n[0] * r[1], work + off[0], norm_dev));
   const double dscale = eps / std::sqrt((double)std::max(d - 1, 1));
