@@ -222,9 +222,9 @@ struct GemmArgs {
 };
 // Structure flags (tiles of 64): only the upper-triangular tiles of C are
 // computed (the strictly lower tiles of C are left unspecified); op(A) / op(B)
-// are upper triangular (kGemmLowA: op(A) lower triangular), so each tile's
-// K range is clipped to the nonzeros.
-constexpr int kGemmUpperC = 1, kGemmTriA = 2, kGemmTriB = 4, kGemmLowA = 8;  // LowA: op(A) lower
+// are upper triangular (kGemmLowA / kGemmLowB: lower triangular), so each
+// tile's K range is clipped to the nonzeros.
+constexpr int kGemmUpperC = 1, kGemmTriA = 2, kGemmTriB = 4, kGemmLowA = 8, kGemmLowB = 16;
 
 int gemm(const GemmArgs& g, cudaStream_t stream);
 

@@ -15,7 +15,10 @@ namespace {
 #ifndef QTT_GEMM_STAGES
 #define QTT_GEMM_STAGES 4
 #endif
-constexpr int BM = 64, BN = 64, BK = 16, PAD = 4, THREADS = 128, STAGES = QTT_GEMM_STAGES;
+#ifndef QTT_GEMM_BK
+#define QTT_GEMM_BK 16
+#endif
+constexpr int BM = 64, BN = 64, BK = QTT_GEMM_BK, PAD = 4, THREADS = 128, STAGES = QTT_GEMM_STAGES;
 constexpr int kGemmSmem = STAGES * BK * (BM + PAD + BN + PAD) * sizeof(double);
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
@@ -58,6 +61,7 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int k
     if (g.flags & kGemmTriA) kbeg = max(kbeg, m0);
     if (g.flags & kGemmTriB) K = min(K, n0 + BN);
     if (g.flags & kGemmLowA) K = min(K, m0 + BM);
+    if (g.flags & kGemmLowB) kbeg = max(kbeg, n0);
   }
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
@@ -333,8 +337,9 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
           const int64_t klo = (g.flags & kGemmTriA) ? (int64_t)mi * BM : 0;
           int64_t khi = (g.flags & kGemmTriB) ? std::min<int64_t>(g.k, (ni + 1) * BN) : g.k;
           if (g.flags & kGemmLowA) khi = std::min<int64_t>(khi, (int64_t)(mi + 1) * BM);
-          if (khi > klo)
-            f += 2.0 * std::min(BM, g.m - mi * BM) * std::min<int64_t>(BN, g.n - ni * BN) * (khi - klo);
+          const int64_t klo2 = (g.flags & kGemmLowB) ? std::max<int64_t>(klo, ni * BN) : klo;
+          if (khi > klo2)
+            f += 2.0 * std::min(BM, g.m - mi * BM) * std::min<int64_t>(BN, g.n - ni * BN) * (khi - klo2);
         }
       f *= g.batch;
     }

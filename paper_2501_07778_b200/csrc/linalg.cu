@@ -626,12 +626,15 @@ __global__ void sum_final_kernel(int nparts, const double* __restrict__ part, do
 }
 
 __global__ void certificate_kernel(int k, const double* rnorm, const double* xnorm,
-                                   const double* delta_dev, double delta_scale, int* ok) {
+                                   const double* delta_dev, double delta_scale, int* ok,
+                                   int debug) {
   const double rn = *rnorm, xn = *xnorm;
   const double delta = delta_dev ? (*delta_dev) * delta_scale : 0.0;
   const double thr = fmax(delta, rn * (double)max(k, 2) * kEps);
-  const bool good = isfinite(xn) && xn > 0.0 && (1.0 / xn) > 1.25 * thr;
+  const bool good = isfinite(xn) && isfinite(rn) && xn > 0.0 && (1.0 / xn) > 1.25 * thr;
   *ok = good ? 1 : 0;
+  if (debug) printf("[cert] k=%d smin/||R||=%.3e thr/||R||=%.3e good=%d\n", k, 1.0 / xn / rn,
+                    thr / rn, (int)good);
 }
 
 __global__ void gather_columns_kernel(int rows, int cols, const double* __restrict__ src,
@@ -957,7 +960,8 @@ int no_truncation_certificate(cudaStream_t s, int k, const double* R, int64_t ld
   QTT_TRY(copy_matrix(s, k, k, R, ldr, Rc, kk));
   QTT_TRY(frob_norm(s, kk * kk, Rc, norms));
   QTT_TRY(frob_norm(s, kk * kk, X, norms + 1));
-  certificate_kernel<<<1, 1, 0, s>>>(k, norms, norms + 1, delta_dev, delta_scale, ok_dev);
+  static const int debug = getenv("QTT_CERT_DEBUG") ? 1 : 0;
+  certificate_kernel<<<1, 1, 0, s>>>(k, norms, norms + 1, delta_dev, delta_scale, ok_dev, debug);
   QTT_CHECK_LAUNCH();
   QTT_CUDA(cudaFreeAsync(Rc, s));
   QTT_CUDA(cudaFreeAsync(X, s));

@@ -30,6 +30,7 @@ int sort_chop(cudaStream_t s, int p, int k, const double* X, int64_t ldx, double
 // Certificate that truncation cannot happen: with R (k x k upper triangular)
 // sets *ok_dev = 1 iff 1/||R^{-1}||_F > 1.25 * max(delta, ||R||_F*max(k,2)*eps),
 // i.e. the smallest singular value of R provably exceeds the _chop threshold.
+// QTT_CERT_DEBUG=1 prints the per-bond margins.
 int no_truncation_certificate(cudaStream_t s, int k, const double* R, int64_t ldr,
                               const double* delta_dev, double delta_scale, int* ok_dev);
 

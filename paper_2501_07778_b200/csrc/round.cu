@@ -11,6 +11,8 @@
 // agree with LAPACK's except at near-ties.  The norm is taken from core 0
 // after orthogonalisation (exact up to rounding, no sqrt(eps) floor).
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "../../include/qtt_b200.h"
@@ -76,7 +78,7 @@ int qr_sweep_right(cudaStream_t s, int d, std::vector<int64_t>& r, const std::ve
   return kOk;
 }
 
-// Left structural reduction: while the left unfolding of core k is wide
+// Left structural reduction: wherever the left unfolding of core k is wide
 // (r_k n_k < r_{k+1}), multiply it into core k+1 and make core k the
 // identity.  Exact (no truncation decision; every bond is still examined by
 // the truncation sweep), and it removes the full-rank Householder/Cholesky
@@ -88,7 +90,7 @@ void reduce_left(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vect
   for (int k = 0; k < d - 1; ++k) {
     const int m = (int)(r[k] * n[k]);
     const int N = (int)r[k + 1];
-    if (m >= N) break;
+    if (m >= N) continue;
     const int mc = (int)(n[k + 1] * r[k + 2]);
     double* core = work + off[k];
     double* next = work + off[k + 1];
@@ -151,7 +153,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
       if (ok) {
         newk = N;
         QTT_TRY(transpose(s, m, N, tq.p, m, core, N));
-        QTT_TRY(dgemm(s, 0, 1, mc, N, N, 1.0, next, mc, tr.p, N, 0.0, tc.p, mc));
+        QTT_TRY(dgemm(s, 0, 1, mc, N, N, 1.0, next, mc, tr.p, N, 0.0, tc.p, mc, kGemmLowB));
       } else {
         QTT_TRY(transpose(s, N, N, tr.p, N, xb.p, N));  // X = R^T
         QTT_TRY(jacobi(s, N, N, xb.p, N, wb.p, N));

@@ -83,11 +83,23 @@ class _TT:
                 raise ValueError("adjacent core ranks do not match")
         dev = _lib.device()
         offs, total = _offsets(shapes)
-        data = torch.zeros(max(total, 1), dtype=torch.float64, device=dev)
-        for c, shp, o in zip(arrs, shapes, offs):
-            t = c if isinstance(c, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(c, dtype=np.float64))
-            n = int(np.prod(shp))
-            data[o : o + n].copy_(t.reshape(-1).to(device=dev, dtype=torch.float64), non_blocking=True)
+        data = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+        on_host = all(not (isinstance(c, torch.Tensor) and c.is_cuda) for c in arrs)
+        if on_host:
+            # pack on the host into one pinned staging buffer, one H2D copy
+            stage = torch.zeros(max(total, 1), dtype=torch.float64, pin_memory=True)
+            sv = stage.numpy()
+            for c, shp, o in zip(arrs, shapes, offs):
+                a = c.detach().numpy() if isinstance(c, torch.Tensor) else c
+                n = int(np.prod(shp))
+                sv[o : o + n] = np.asarray(a, dtype=np.float64).reshape(-1)
+            data.copy_(stage, non_blocking=True)
+        else:
+            data.zero_()
+            for c, shp, o in zip(arrs, shapes, offs):
+                t = c if isinstance(c, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(c, dtype=np.float64))
+                n = int(np.prod(shp))
+                data[o : o + n].copy_(t.reshape(-1).to(device=dev, dtype=torch.float64), non_blocking=True)
         self.data = data
         self._shapes = tuple(shapes)
         self._offs = offs
@@ -108,7 +120,12 @@ class _TT:
         )
 
     def numpy_cores(self) -> list:
-        return [c.detach().cpu().numpy() for c in self.cores]
+        """Host copies of the cores: one D2H copy of the packed buffer into
+        pinned memory, returned as numpy views of it."""
+        host = torch.empty(self.data.numel(), dtype=torch.float64, pin_memory=True)
+        host.copy_(self.data)
+        hv = host.numpy()
+        return [hv[o : o + int(np.prod(s))].reshape(s) for o, s in zip(self._offs, self._shapes)]
 
     @property
     def d(self) -> int:
