@@ -12,14 +12,26 @@
 namespace qtt {
 namespace {
 
-#ifndef QTT_GEMM_STAGES
-#define QTT_GEMM_STAGES 4
+constexpr int BK = 16, PAD = 4;
+
+// CTA tile configurations: WM x WN warps, each owning a (8 TM) x (8 TN) block
+// of DMMA m8n8 tiles; CTA tile (8 WM TM) x (8 WN TN); STG-deep pipeline.
+template <int WM_, int WN_, int TM_, int TN_, int STG_>
+struct TileCfg {
+  static constexpr int WM = WM_, WN = WN_, TM = TM_, TN = TN_, STG = STG_;
+  static constexpr int BM = 8 * WM * TM, BN = 8 * WN * TN, THREADS = 32 * WM * WN;
+  static constexpr int SMEM = STG * BK * (BM + PAD + BN + PAD) * (int)sizeof(double);
+  static_assert(STG >= 3, "pipeline needs >= 3 stages");
+};
+using CfgSmall = TileCfg<2, 2, 4, 4, 4>;  // 64 x 64, 4 warps
+#ifndef QTT_BIG_WM
+#define QTT_BIG_WM 2
+#define QTT_BIG_WN 2
+#define QTT_BIG_TM 4
+#define QTT_BIG_TN 4
+#define QTT_BIG_STG 4
 #endif
-#ifndef QTT_GEMM_BK
-#define QTT_GEMM_BK 16
-#endif
-constexpr int BM = 64, BN = 64, BK = QTT_GEMM_BK, PAD = 4, THREADS = 128, STAGES = QTT_GEMM_STAGES;
-constexpr int kGemmSmem = STAGES * BK * (BM + PAD + BN + PAD) * sizeof(double);
+using CfgBig = TileCfg<QTT_BIG_WM, QTT_BIG_WN, QTT_BIG_TM, QTT_BIG_TN, QTT_BIG_STG>;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -37,15 +49,24 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-template <int TA, int TB>
-__global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int kchunk, double* ws) {
+template <int TA, int TB, class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS) gemm_kernel(GemmArgs g, int mt, int kchunk, double* ws) {
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, THREADS = Cfg::THREADS, STAGES = Cfg::STG;
+  constexpr int TM = Cfg::TM, TN = Cfg::TN;
   extern __shared__ double gemm_sm[];
   double (*As)[BK][BM + PAD] = reinterpret_cast<double (*)[BK][BM + PAD]>(gemm_sm);
   double (*Bs)[BK][BN + PAD] = reinterpret_cast<double (*)[BK][BN + PAD]>(gemm_sm + STAGES * BK * (BM + PAD));
 
+  // Grouped tile order: consecutive CTAs cover GROUP m-tiles x all n-tiles
+  // column by column, so the A panels of a wave stay in L2.
+  constexpr int GROUP = 8;
   const int tile = blockIdx.x;
-  const int m0 = (tile % mt) * BM;
-  const int n0 = (tile / mt) * BN;
+  const int nt = (g.n + BN - 1) / BN;
+  const int first_m = (tile / (GROUP * nt)) * GROUP;
+  const int gsz = min(mt - first_m, GROUP);
+  const int in_group = tile % (GROUP * nt);
+  const int m0 = (first_m + in_group % gsz) * BM;
+  const int n0 = (in_group / gsz) * BN;
   const int bz = blockIdx.y;
   const double* A = g.a + bz * g.stride_a;
   const double* B = g.b + bz * g.stride_b;
@@ -54,7 +75,7 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int k
   int kbeg = blockIdx.z * kchunk;
   int K = min(g.k, kbeg + kchunk);  // tiles cover [kbeg, K)
   if (g.flags) {
-    if ((g.flags & kGemmUpperC) && m0 > n0) {
+    if ((g.flags & kGemmUpperC) && m0 >= n0 + BN) {
       if (ws == nullptr) return;
       K = kbeg;  // split-K partial of a skipped tile: zeros
     }
@@ -64,65 +85,110 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int k
     if (g.flags & kGemmLowB) kbeg = max(kbeg, n0);
   }
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  const int wm = (warp % Cfg::WM) * (8 * TM), wn = (warp / Cfg::WM) * (8 * TN);
 
-  auto load_tile = [&](int buf, int k0) {
+  // Global -> shared tile loads.  Every thread owns a fixed row (or column)
+  // of the tile and a fixed set of k offsets, so the addresses are one base
+  // pointer plus compile-time multiples of a precomputed stride, and the
+  // row predicate is hoisted; only the K bound is tested per stage.
+  static_assert(THREADS % BM == 0 && THREADS % BN == 0 && THREADS % BK == 0, "tile/thread shape");
+  constexpr int A_E = (BM * BK) / THREADS, B_E = (BN * BK) / THREADS;
+  // TA == 0: A(m, k) at a + m + k lda, thread -> m = t % BM, k = t / BM + e (THREADS / BM)
+  // TA == 1: A(m, k) at a + k + m lda, thread -> k = t % BK, m = t / BK + e (THREADS / BK)
+  const int a_m = TA == 0 ? t % BM : t / BK, a_k = TA == 0 ? t / BM : t % BK;
+  const int b_n = TB == 0 ? t / BK : t % BN, b_k = TB == 0 ? t % BK : t / BN;
+  const double* pa = A + (TA == 0 ? (int64_t)(m0 + a_m) + (int64_t)(kbeg + a_k) * g.lda
+                                   : (int64_t)(kbeg + a_k) + (int64_t)(m0 + a_m) * g.lda);
+  const double* pb = B + (TB == 0 ? (int64_t)(kbeg + b_k) + (int64_t)(n0 + b_n) * g.ldb
+                                   : (int64_t)(n0 + b_n) + (int64_t)(kbeg + b_k) * g.ldb);
+  const int64_t a_es = TA == 0 ? (int64_t)(THREADS / BM) * g.lda : (int64_t)(THREADS / BK) * g.lda;
+  const int64_t b_es = TB == 0 ? (int64_t)(THREADS / BK) * g.ldb : (int64_t)(THREADS / BN) * g.ldb;
+  const int64_t a_ks = TA == 0 ? (int64_t)BK * g.lda : BK;  // per stage
+  const int64_t b_ks = TB == 0 ? BK : (int64_t)BK * g.ldb;
+  // row predicates (TA == 1 / TB == 0: the owned rows/columns vary with e)
+  unsigned a_rows = 0, b_cols = 0;
 #pragma unroll
-    for (int e = 0; e < (BM * BK) / THREADS; ++e) {
-      int idx = t + e * THREADS;
-      int mm, kk;
-      if (TA == 0) { mm = idx % BM; kk = idx / BM; } else { kk = idx % BK; mm = idx / BK; }
-      int gm = m0 + mm, gk = k0 + kk;
-      bool ok = gm < M && gk < K;
-      const double* src = ok ? (TA == 0 ? A + gm + (int64_t)gk * g.lda : A + gk + (int64_t)gm * g.lda) : A;
-      cp_async8(&As[buf][kk][mm], src, ok);
+  for (int e = 0; e < A_E; ++e) {
+    const int m = TA == 0 ? a_m : a_m + e * (THREADS / BK);
+    if (m0 + m < M) a_rows |= 1u << e;
+  }
+#pragma unroll
+  for (int e = 0; e < B_E; ++e) {
+    const int nn = TB == 0 ? b_n + e * (THREADS / BK) : b_n;
+    if (n0 + nn < N) b_cols |= 1u << e;
+  }
+  auto load_tile = [&](int buf, int st) {
+    const int k0 = kbeg + st * BK;
+    const double* qa = pa + st * a_ks;
+    const double* qb = pb + st * b_ks;
+#pragma unroll
+    for (int e = 0; e < A_E; ++e) {
+      const int kk = TA == 0 ? a_k + e * (THREADS / BM) : a_k;
+      const int mm = TA == 0 ? a_m : a_m + e * (THREADS / BK);
+      const bool ok = ((a_rows >> e) & 1u) && k0 + kk < K;
+      cp_async8(&As[buf][kk][mm], ok ? qa + e * a_es : A, ok);
     }
 #pragma unroll
-    for (int e = 0; e < (BN * BK) / THREADS; ++e) {
-      int idx = t + e * THREADS;
-      int nn, kk;
-      if (TB == 0) { kk = idx % BK; nn = idx / BK; } else { nn = idx % BN; kk = idx / BN; }
-      int gn = n0 + nn, gk = k0 + kk;
-      bool ok = gn < N && gk < K;
-      const double* src = ok ? (TB == 0 ? B + gk + (int64_t)gn * g.ldb : B + gn + (int64_t)gk * g.ldb) : B;
-      cp_async8(&Bs[buf][kk][nn], src, ok);
+    for (int e = 0; e < B_E; ++e) {
+      const int kk = TB == 0 ? b_k : b_k + e * (THREADS / BN);
+      const int nn = TB == 0 ? b_n + e * (THREADS / BK) : b_n;
+      const bool ok = ((b_cols >> e) & 1u) && k0 + kk < K;
+      cp_async8(&Bs[buf][kk][nn], ok ? qb + e * b_es : B, ok);
     }
   };
 
-  double acc[4][4][2];
+  double acc[TM][TN][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int ktiles = (K - kbeg + BK - 1) / BK;
-  // STAGES-deep cp.async pipeline: tiles kt+1 .. kt+STAGES-1 are in flight
-  // while tile kt is multiplied (one commit group per tile, empty groups at
-  // the tail keep the wait count uniform).
+  // STAGES-deep cp.async pipeline (one commit group per stage; empty groups
+  // at the tail keep the wait counts uniform) with register double-buffered
+  // fragments: the fragments of k-step s+1 are loaded while the DMMAs of
+  // k-step s issue; the single barrier per stage sits before the last
+  // k-step, when the next stage's first fragments are fetched.
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) {
-    if (st < ktiles) load_tile(st, kbeg + st * BK);
+    if (st < ktiles) load_tile(st, st);
     cp_async_commit();
   }
-  for (int kt = 0; kt < ktiles; ++kt) {
+  constexpr int KS = BK / 4;
+  double af[2][TM], bf[2][TN];
+  auto load_frag = [&](int buf, int ks, int slot) {
+    const int kr = ks * 4 + (lane & 3);
+#pragma unroll
+    for (int i = 0; i < TM; ++i) af[slot][i] = As[buf][kr][wm + i * 8 + (lane >> 2)];
+#pragma unroll
+    for (int j = 0; j < TN; ++j) bf[slot][j] = Bs[buf][kr][wn + j * 8 + (lane >> 2)];
+  };
+  if (ktiles > 0) {
     cp_async_wait<STAGES - 2>();
-    __syncthreads();  // tile kt landed for all threads; buffer (kt-1) % STAGES is free
-    const int nxt = kt + STAGES - 1;
-    if (nxt < ktiles) load_tile(nxt % STAGES, kbeg + nxt * BK);
-    cp_async_commit();
+    __syncthreads();
+    load_frag(0, 0, 0);
+  }
+  for (int kt = 0; kt < ktiles; ++kt) {
     const int buf = kt % STAGES;
 #pragma unroll
-    for (int ks = 0; ks < BK; ks += 4) {
-      double af[4], bf[4];
-      const int kr = ks + (lane & 3);
+    for (int ks = 0; ks < KS; ++ks) {
+      const int cur = ks & 1;
+      if (ks == KS - 1) {
+        // stage kt+1 landed (groups 0..kt+STAGES-2 committed) and every
+        // thread is past its reads of stage kt-1, whose buffer is refilled
+        cp_async_wait<STAGES - 3>();
+        __syncthreads();
+        const int nxt = kt + STAGES - 1;
+        if (nxt < ktiles) load_tile(nxt % STAGES, nxt);
+        cp_async_commit();
+        if (kt + 1 < ktiles) load_frag((kt + 1) % STAGES, 0, cur ^ 1);
+      } else {
+        load_frag(buf, ks + 1, cur ^ 1);
+      }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = As[buf][kr][wm + i * 8 + (lane >> 2)];
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][kr][wn + j * 8 + (lane >> 2)];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < TN; ++j) dmma(acc[i][j], af[cur][i], bf[cur][j]);
     }
   }
   cp_async_wait<0>();
@@ -131,11 +197,11 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int k
     // split-K partial: plain accumulator into ws[(z * batch + b) * M * N]
     double* W = ws + ((int64_t)blockIdx.z * gridDim.y + bz) * (int64_t)M * N;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < TM; ++i) {
       const int row = m0 + wm + i * 8 + (lane >> 2);
       if (row >= M) continue;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < TN; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int col = n0 + wn + j * 8 + 2 * (lane & 3) + h;
@@ -147,12 +213,12 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int k
   const double alpha = g.alpha, beta = g.beta;
   if (beta != 0.0) {
     // all C loads in flight before the first store (no load-store chain)
-    double cv[4][4][2];
+    double cv[TM][TN][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < TM; ++i) {
       const int row = m0 + wm + i * 8 + (lane >> 2);
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < TN; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int col = n0 + wn + j * 8 + 2 * (lane & 3) + h;
@@ -160,25 +226,25 @@ __global__ void __launch_bounds__(THREADS) gemm_kernel(GemmArgs g, int mt, int k
         }
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < TM; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < TN; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) acc[i][j][h] = fma(alpha, acc[i][j][h], beta * cv[i][j][h]);
   } else {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < TM; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < TN; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) acc[i][j][h] *= alpha;
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < TM; ++i) {
     const int row = m0 + wm + i * 8 + (lane >> 2);
     if (row >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < TN; ++j) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int col = n0 + wn + j * 8 + 2 * (lane & 3) + h;
@@ -279,6 +345,11 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
     QTT_CHECK_LAUNCH();
     return kOk;
   }
+  // Large CTA tiles when they still fill the GPU (fewer smem bytes per
+  // DMMA), 64 x 64 tiles for small / skinny products.
+  const bool big = ceil_div(g.m, CfgBig::BM) * ceil_div(g.n, CfgBig::BN) * g.batch >= 2 * num_sms() &&
+                   g.k >= 128 && !getenv("QTT_GEMM_SMALL_ONLY");
+  const int BM = big ? CfgBig::BM : CfgSmall::BM, BN = big ? CfgBig::BN : CfgSmall::BN;
   const int mt = (int)ceil_div(g.m, BM);
   const int64_t tiles = (int64_t)mt * ceil_div(g.n, BN);
   if (tiles > 0x7fffffff) return kUnsupported;
@@ -307,16 +378,24 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
   grid.z = splits;
   static bool configured = false;
   if (!configured) {
-    QTT_CUDA(cudaFuncSetAttribute(gemm_kernel<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem));
-    QTT_CUDA(cudaFuncSetAttribute(gemm_kernel<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem));
-    QTT_CUDA(cudaFuncSetAttribute(gemm_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem));
-    QTT_CUDA(cudaFuncSetAttribute(gemm_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmem));
+#define QTT_CFG_ATTR(TA_, TB_, CF)                                                                   \
+  QTT_CUDA(cudaFuncSetAttribute(gemm_kernel<TA_, TB_, CF>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                CF::SMEM));
+    QTT_CFG_ATTR(0, 0, CfgSmall) QTT_CFG_ATTR(0, 1, CfgSmall) QTT_CFG_ATTR(1, 0, CfgSmall) QTT_CFG_ATTR(1, 1, CfgSmall)
+    QTT_CFG_ATTR(0, 0, CfgBig) QTT_CFG_ATTR(0, 1, CfgBig) QTT_CFG_ATTR(1, 0, CfgBig) QTT_CFG_ATTR(1, 1, CfgBig)
+#undef QTT_CFG_ATTR
     configured = true;
   }
-  if (!g.trans_a && !g.trans_b) gemm_kernel<0, 0><<<grid, THREADS, kGemmSmem, stream>>>(g, mt, kchunk, ws);
-  else if (!g.trans_a && g.trans_b) gemm_kernel<0, 1><<<grid, THREADS, kGemmSmem, stream>>>(g, mt, kchunk, ws);
-  else if (g.trans_a && !g.trans_b) gemm_kernel<1, 0><<<grid, THREADS, kGemmSmem, stream>>>(g, mt, kchunk, ws);
-  else gemm_kernel<1, 1><<<grid, THREADS, kGemmSmem, stream>>>(g, mt, kchunk, ws);
+#define QTT_LAUNCH(CF)                                                                             \
+  do {                                                                                             \
+    if (!g.trans_a && !g.trans_b) gemm_kernel<0, 0, CF><<<grid, CF::THREADS, CF::SMEM, stream>>>(g, mt, kchunk, ws); \
+    else if (!g.trans_a && g.trans_b) gemm_kernel<0, 1, CF><<<grid, CF::THREADS, CF::SMEM, stream>>>(g, mt, kchunk, ws); \
+    else if (g.trans_a && !g.trans_b) gemm_kernel<1, 0, CF><<<grid, CF::THREADS, CF::SMEM, stream>>>(g, mt, kchunk, ws); \
+    else gemm_kernel<1, 1, CF><<<grid, CF::THREADS, CF::SMEM, stream>>>(g, mt, kchunk, ws);       \
+  } while (0)
+  if (big) QTT_LAUNCH(CfgBig);
+  else QTT_LAUNCH(CfgSmall);
+#undef QTT_LAUNCH
   QTT_CHECK_LAUNCH();
   if (splits > 1) {
     const int64_t total = (int64_t)g.m * g.n * g.batch;
@@ -333,7 +412,7 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
       f = 0.0;
       for (int mi = 0; mi < mt; ++mi)
         for (int64_t ni = 0; ni < tiles / mt; ++ni) {
-          if ((g.flags & kGemmUpperC) && mi > ni) continue;
+          if ((g.flags & kGemmUpperC) && (int64_t)mi * BM >= (ni + 1) * BN) continue;
           const int64_t klo = (g.flags & kGemmTriA) ? (int64_t)mi * BM : 0;
           int64_t khi = (g.flags & kGemmTriB) ? std::min<int64_t>(g.k, (ni + 1) * BN) : g.k;
           if (g.flags & kGemmLowA) khi = std::min<int64_t>(khi, (int64_t)(mi + 1) * BM);
