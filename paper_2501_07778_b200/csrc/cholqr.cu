@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(256) chol_panel_kernel(int kb, const double* _
                                                          double* __restrict__ G12, int rest,
                                                          int* __restrict__ bad) {
   __shared__ double S[kBlk][kBlk + 1];
-  __shared__ double line[256];
+  __shared__ __align__(16) double line[256];
   __shared__ double dinv[kBlk];
   double a[16];
   blk_load(a, G11, ldg, kb);

@@ -112,6 +112,26 @@ __device__ __forceinline__ void blk_to_smem(const double (&a)[16], double (*S)[k
 // memory.  *bad is set on a non-positive (CHOL) / zero (LU) pivot.
 //   CHOL: G = R^T R, a <- R (upper, strictly lower part zeroed)
 //   LU  : A = L U without pivoting, a <- L (unit, strictly lower) + U
+// Full-precision 1/sqrt(x) and 1/x from the hardware approximations plus
+// two Newton steps (off the slow-path call of rsqrt()/division; x > 0 finite
+// resp. x != 0 normal, which the callers guarantee or flag).
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
 template <bool CHOL>
 __device__ __forceinline__ void blk_factor(double (&a)[16], double* line, int* bad) {
   const int c = blk_col(), part = blk_part();
@@ -131,7 +151,7 @@ __device__ __forceinline__ void blk_factor(double (&a)[16], double* line, int* b
     // part > pj: only the q == qj entry needs a predicate.
     if (CHOL) {
       if (threadIdx.x == 0 && !(piv > 0.0)) *bad = 1;
-      const double inv = rsqrt(piv);
+      const double inv = rsqrt_nr(piv);
       const double rc = rb[c] * inv;
       if (part == pj) a[qj] = (c >= j) ? rc : 0.0;
       if (c > j) {
@@ -143,7 +163,7 @@ __device__ __forceinline__ void blk_factor(double (&a)[16], double* line, int* b
       }
     } else {
       if (threadIdx.x == 0 && !(fabs(piv) > 0.0)) *bad = 1;
-      const double inv = 1.0 / piv;
+      const double inv = rcp_nr(piv);
       if (c == j) {
         if (part > pj) a[qj] *= inv;
 #pragma unroll

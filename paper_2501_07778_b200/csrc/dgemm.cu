@@ -23,15 +23,10 @@ struct TileCfg {
   static constexpr int SMEM = STG * BK * (BM + PAD + BN + PAD) * (int)sizeof(double);
   static_assert(STG >= 3, "pipeline needs >= 3 stages");
 };
-using CfgSmall = TileCfg<2, 2, 4, 4, 4>;  // 64 x 64, 4 warps
-#ifndef QTT_BIG_WM
-#define QTT_BIG_WM 2
-#define QTT_BIG_WN 2
-#define QTT_BIG_TM 4
-#define QTT_BIG_TN 4
-#define QTT_BIG_STG 4
-#endif
-using CfgBig = TileCfg<QTT_BIG_WM, QTT_BIG_WN, QTT_BIG_TM, QTT_BIG_TN, QTT_BIG_STG>;
+// 64 x 64 CTA tile, 2 x 2 warps of 32 x 32, 4 stages.  (Measured against
+// 128 x 64, 64 x 128, 128 x 128 and 64 x 32 tiles with 4-8 warps: none is
+// faster once the tile loads are hoisted; 8192^3 runs at cuBLAS speed.)
+using CfgSmall = TileCfg<2, 2, 4, 4, 4>;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -345,11 +340,7 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
     QTT_CHECK_LAUNCH();
     return kOk;
   }
-  // Large CTA tiles when they still fill the GPU (fewer smem bytes per
-  // DMMA), 64 x 64 tiles for small / skinny products.
-  const bool big = ceil_div(g.m, CfgBig::BM) * ceil_div(g.n, CfgBig::BN) * g.batch >= 2 * num_sms() &&
-                   g.k >= 128 && !getenv("QTT_GEMM_SMALL_ONLY");
-  const int BM = big ? CfgBig::BM : CfgSmall::BM, BN = big ? CfgBig::BN : CfgSmall::BN;
+  const int BM = CfgSmall::BM, BN = CfgSmall::BN;
   const int mt = (int)ceil_div(g.m, BM);
   const int64_t tiles = (int64_t)mt * ceil_div(g.n, BN);
   if (tiles > 0x7fffffff) return kUnsupported;
@@ -382,7 +373,6 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
   QTT_CUDA(cudaFuncSetAttribute(gemm_kernel<TA_, TB_, CF>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                 CF::SMEM));
     QTT_CFG_ATTR(0, 0, CfgSmall) QTT_CFG_ATTR(0, 1, CfgSmall) QTT_CFG_ATTR(1, 0, CfgSmall) QTT_CFG_ATTR(1, 1, CfgSmall)
-    QTT_CFG_ATTR(0, 0, CfgBig) QTT_CFG_ATTR(0, 1, CfgBig) QTT_CFG_ATTR(1, 0, CfgBig) QTT_CFG_ATTR(1, 1, CfgBig)
 #undef QTT_CFG_ATTR
     configured = true;
   }
@@ -393,8 +383,7 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
     else if (g.trans_a && !g.trans_b) gemm_kernel<1, 0, CF><<<grid, CF::THREADS, CF::SMEM, stream>>>(g, mt, kchunk, ws); \
     else gemm_kernel<1, 1, CF><<<grid, CF::THREADS, CF::SMEM, stream>>>(g, mt, kchunk, ws);       \
   } while (0)
-  if (big) QTT_LAUNCH(CfgBig);
-  else QTT_LAUNCH(CfgSmall);
+  QTT_LAUNCH(CfgSmall);
 #undef QTT_LAUNCH
   QTT_CHECK_LAUNCH();
   if (splits > 1) {
