@@ -67,6 +67,11 @@ int qtt_profile_gemm_read(double* flops, double* ms, int64_t* launches);
 /* Number of doubles a packed buffer for `lay` needs (with alignment). */
 int64_t qtt_layout_size(const qtt_layout* lay);
 
+/* Synchronise `stream` and return the unused memory cached by the library's
+ * stream-ordered pool to the driver (no reference counterpart: host-side
+ * memory management for growing AMEn local systems, solver.py:148-171). */
+int qtt_release_cached(void* stream);
+
 /* ---------------------------------------------------------------- (a2,a3)
  * Exact core-wise products, all cores in ONE launch.
  * qtt_matvec  replaces ttcore.tt_matvec  (ttcore.py:443-455):

@@ -26,6 +26,7 @@ EXPORTS = (
     "qtt_profile_gemm",
     "qtt_profile_gemm_read",
     "qtt_layout_size",
+    "qtt_release_cached",
     "qtt_matvec",
     "qtt_matmat",
     "qtt_hadamard",
@@ -135,6 +136,17 @@ def align(n: int) -> int:
 
 def launch_count() -> int:
     return int(load().qtt_launch_count())
+
+
+def release_cached() -> None:
+    """Return cached device memory of BOTH allocators (torch's caching
+    allocator and the library's stream-ordered pool) to the driver.  The two
+    caches cannot serve each other, so when allocations grow step by step
+    (AMEn local systems of tens of GB) each must be trimmed before the other
+    allocates."""
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    call("qtt_release_cached", stream_handle())
 
 
 def gemm_profile_start() -> None:

@@ -1,5 +1,7 @@
 // extern "C" boundary of libqttb200.so (declared in include/qtt_b200.h).
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/qtt_b200.h"
@@ -82,6 +84,7 @@ int qtt_profile_gemm(int32_t on) {
   }
   p.events.clear();
   p.launch_flops.clear();
+  p.shapes.clear();
   p.flops = 0.0;
   p.on = on != 0;
   return QTT_OK;
@@ -97,9 +100,28 @@ int qtt_profile_gemm_read(double* flops, double* ms, int64_t* launches) {
     QTT_CUDA(cudaEventElapsedTime(&t, e.first, e.second));
     tot += t;
   }
+  if (getenv("QTT_GEMM_LOG"))  // per-launch shapes for tools/gemm_shapes.py
+    for (size_t i = 0; i < p.events.size() && i < p.shapes.size(); ++i) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, p.events[i].first, p.events[i].second);
+      const auto& q = p.shapes[i];
+      fprintf(stderr, "[gemm] %ld %ld %ld %ld %ld %ld %.4f %.6e\n", (long)q[0], (long)q[1], (long)q[2],
+              (long)q[3], (long)q[4], (long)q[5], t, p.launch_flops[i]);
+    }
   *flops = p.flops;
   *ms = tot;
   *launches = (int64_t)p.events.size();
+  return QTT_OK;
+}
+
+int qtt_release_cached(void* stream) {
+  pool_init();
+  QTT_CUDA(cudaStreamSynchronize(S(stream)));
+  int dev = 0;
+  QTT_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  QTT_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  QTT_CUDA(cudaMemPoolTrimTo(pool, 0));
   return QTT_OK;
 }
 

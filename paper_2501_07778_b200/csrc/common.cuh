@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <algorithm>
 #include <utility>
+#include <array>
 #include <vector>
 
 namespace qtt {
@@ -261,6 +262,7 @@ struct GemmProfile {
   double flops = 0.0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
   std::vector<double> launch_flops;
+  std::vector<std::array<int64_t, 6>> shapes;  // m, n, k, batch, flags, splits
 };
 GemmProfile& gemm_profile();
 

@@ -412,6 +412,7 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
       f *= g.batch;
     }
     prof.launch_flops.push_back(f);
+    prof.shapes.push_back({g.m, g.n, g.k, g.batch, g.flags, splits});
     prof.flops += f;
   }
   return kOk;

@@ -39,7 +39,10 @@ from .ttcore import (
 
 __all__ = ["SolverConfig", "SolveOutcome", "solve", "residual", "apply_tt_matrix"]
 
+_RELEASE_DIM = 12000  # local systems above ~1.1 GB trim the allocator caches first
 _DENSE_LOCAL_LIMIT = 1200  # kept for API parity (solver.py:23); local solves are direct
+
+_TRACE = bool(__import__("os").environ.get("QTT_AMEN_TRACE"))
 
 # Optional phase timing (synchronising; diagnostics only): set PROFILE = {}.
 PROFILE = None
@@ -70,6 +73,12 @@ class SolverConfig:
     seed: int = 0
     trunc_factor: float = 0.5
     max_rank: int = 400
+    # "reference": SVD truncation at delta with the stall adaptation of
+    # solver.py:374-380 (drop-in behaviour).  "residual": the AMEn
+    # local-residual rule (Dolgov & Savostyanov 2014): keep the smallest rank
+    # whose truncated local solution still satisfies the local system to
+    # trunc_factor * epsilon / sqrt(d) (no stall adaptation needed).
+    truncation: str = "reference"
 
     def __post_init__(self):
         if self.epsilon <= 0:
@@ -78,6 +87,8 @@ class SolverConfig:
             raise ValueError("max_sweeps must be >= 1")
         if self.local_solver not in ("auto", "direct", "iterative"):
             raise ValueError(f"unknown local solver {self.local_solver!r}")
+        if self.truncation not in ("reference", "residual"):
+            raise ValueError(f"unknown truncation rule {self.truncation!r}")
 
 
 @dataclass(frozen=True)
@@ -191,13 +202,19 @@ def _local_matrix_cm(phi_l, a_p, phi_r):
     return mat.view(-1)
 
 
-def _solve_local(phi_l, a_p, phi_r, rhs):
+def _solve_local(phi_l, a_p, phi_r, rhs, keep=False):
     rl, n, rr = rhs.shape
     dim = rl * n * rr
+    if dim > _RELEASE_DIM:
+        # local systems grow sweep by sweep; stale blocks of either cache
+        # would otherwise pin tens of GB (see _lib.release_cached)
+        _lib.release_cached()
     with _phase("local_matrix"):
         mcm = _local_matrix_cm(phi_l, a_p, phi_r)
     with _phase("local_lu"):
         sol, _ = dense_solve_colmajor(mcm, dim, rhs.reshape(-1))
+    if keep:
+        return sol.view(rl, n, rr), mcm
     return sol.view(rl, n, rr)
 
 
@@ -245,6 +262,29 @@ def _truncated_split_right(core, delta, rmax):
     return vr.contiguous(), carry
 
 
+def _residual_split_right(core, mcm, rhs, tol, rmax):
+    """Local-residual truncation: the smallest r whose truncated core
+    x_r = core V_r V_r^T keeps ||M x_r - rhs|| <= max(tol ||rhs||, 2 ||M x - rhs||).
+    All candidate residuals come from one GEMM: row i of W is M applied to the
+    rank-one increment (core v_i) v_i^T, and x_r's residual is rhs - sum_{i<r} W_i."""
+    rl, n, rr = core.shape
+    dim = rl * n * rr
+    s, v, k = svd_left_colmajor(core.contiguous().view(-1), n * rr, rl)
+    vk = v.view(k, n * rr)
+    carry_all = mm(core.reshape(rl, n * rr), vk, tb=True)  # (rl, k) = U S
+    inc = carry_all.t().unsqueeze(2) * vk.unsqueeze(1)  # (k, rl, n rr)
+    w = mm(inc.reshape(k, dim), mcm.view(dim, dim))  # rows: (M inc_i)^T
+    resid = rhs.reshape(1, dim) - torch.cumsum(w, dim=0)
+    rn = torch.linalg.vector_norm(resid, dim=1).cpu().numpy()
+    bn = float(torch.linalg.vector_norm(rhs))
+    target = max(tol * bn, 2.0 * rn[-1])
+    ok = np.nonzero(rn <= target)[0]
+    r = int(ok[0] + 1) if ok.size else k
+    r = max(1, min(r, rmax))
+    vr = vk[:r].contiguous().view(r, n, rr)
+    return vr, carry_all[:, :r].contiguous()
+
+
 def _safe_core(core, rng):
     if float(torch.linalg.vector_norm(core)) == 0.0:
         return torch.from_numpy(np.asarray(rng.standard_normal(tuple(core.shape))) * 1e-30).to(core.device)
@@ -286,8 +326,11 @@ def _operator_views(K: TTMatrix):
 # ------------------------------------------------------------------ solve
 
 
-def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig) -> SolveOutcome:
-    """AMEn-style alternating solve of K u = f (solver.py:239-389)."""
+def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig, x0: TTVector | None = None) -> SolveOutcome:
+    """AMEn-style alternating solve of K u = f (solver.py:239-389).
+
+    ``x0`` (extension, not in the reference API): initial guess replacing the
+    seeded rank-2 start; the enrichment cores are still drawn from the seed."""
     if K.col_mode_sizes != f.mode_sizes or K.row_mode_sizes != f.mode_sizes:
         raise ValueError("operator and right-hand side modes do not match")
     t0 = time.perf_counter()
@@ -303,6 +346,10 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig) -> SolveOutcome:
     rho = cfg.enrichment_rank
     x = _init_cores(rng, sizes, 2, dev)
     z = _init_cores(rng, sizes, rho, dev)
+    if x0 is not None:
+        if x0.mode_sizes != sizes:
+            raise ValueError("initial guess modes do not match the right-hand side")
+        x = _right_orthogonalize_all([c.contiguous().clone() for c in x0.cores])
     A = _operator_views(K)
     F = [c.contiguous() for c in f.cores]
 
@@ -327,6 +374,8 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig) -> SolveOutcome:
     rank_history, residual_history = [], []
     res, res_prev = np.inf, np.inf
     adapt = 1.0
+    residual_rule = cfg.truncation == "residual"
+    tol_loc = cfg.trunc_factor * cfg.epsilon / np.sqrt(d)
     sweeps_done = 0
     for sweep in range(cfg.max_sweeps):
         # ---------------- forward: solve + enrich ----------------
@@ -356,10 +405,14 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig) -> SolveOutcome:
         delta = cfg.trunc_factor * cfg.epsilon * adapt * max(xnorm, 1e-300) / np.sqrt(d)
         for k in range(d - 1, -1, -1):
             rhs = _local_rhs(psi_l[k], F[k], psi_r[k + 1])
-            xk = _solve_local(phi_l[k], A[k], phi_r[k + 1], rhs)
+            xk, mcm = _solve_local(phi_l[k], A[k], phi_r[k + 1], rhs, keep=True)
             if k > 0:
                 with _phase("svd_split"):
-                    x[k], carry = _truncated_split_right(xk, delta, cfg.max_rank)
+                    if residual_rule:
+                        x[k], carry = _residual_split_right(xk, mcm, rhs, tol_loc, cfg.max_rank)
+                    else:
+                        x[k], carry = _truncated_split_right(xk, delta, cfg.max_rank)
+                del mcm
                 p0, pn, p1 = x[k - 1].shape
                 x[k - 1] = mm(x[k - 1].reshape(p0 * pn, p1), carry).view(p0, pn, carry.shape[1])
                 phi_r[k] = _phi_right(phi_r[k + 1], x[k], A[k], x[k])
@@ -375,9 +428,12 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig) -> SolveOutcome:
         with _phase("residual"):
             res = residual(K, u, f)
         residual_history.append(float(res))
+        if _TRACE:
+            print(f"[amen] sweep {sweep + 1} res {res:.3e} max rank {rank_history[-1]} "
+                  f"t {time.perf_counter() - t0:.2f}s", flush=True)
         if res <= cfg.epsilon:
             break
-        if res > 0.7 * res_prev and adapt > 2.0**-44:
+        if not residual_rule and res > 0.7 * res_prev and adapt > 2.0**-44:
             adapt *= 0.25
         res_prev = res
 

@@ -38,15 +38,17 @@ def global_system(name):
                              epsilon=spec["eps"]), spec
 
 
+@pytest.mark.parametrize("truncation", ["reference", "residual"])
 @pytest.mark.parametrize("name", ["single3", "lshape2", "cantilever2"])
-def test_solve_matches_reference(name):
+def test_solve_matches_reference(name, truncation):
     from paper_2501_07778_b200 import solver as S
     from paper_2501_07778_b200.ttcore import tt_contract
 
     g = load("coupling")
     gsys, spec = global_system(name)
     eps = spec["solve"]
-    out = S.solve(gsys.K, gsys.f, S.SolverConfig(epsilon=eps, seed=0, local_solver="direct"))
+    out = S.solve(gsys.K, gsys.f, S.SolverConfig(epsilon=eps, seed=0, local_solver="direct",
+                                                 truncation=truncation))
     assert out.converged
     assert out.residual <= eps
     kd, fd = g[f"{name}_Kd"], g[f"{name}_fd"]
