@@ -69,7 +69,10 @@ class SolverConfig:
     epsilon: float = 1e-8
     max_sweeps: int = 40
     enrichment_rank: int = 4
-    local_solver: str = "auto"  # direct | iterative | auto  (all use the device LU)
+    # direct: dense device LU for every local system; iterative/auto: device
+    # GMRES (warm start, restart 40, reference tolerance) above
+    # _ITERATIVE_MIN_DIM unknowns, dense LU below and as fallback
+    local_solver: str = "auto"
     seed: int = 0
     trunc_factor: float = 0.5
     max_rank: int = 400
@@ -202,9 +205,108 @@ def _local_matrix_cm(phi_l, a_p, phi_r):
     return mat.view(-1)
 
 
-def _solve_local(phi_l, a_p, phi_r, rhs, keep=False):
+_LOCAL_HOOK = None  # diagnostics: called with (phi_l, a_p, phi_r, rhs, x_cur, sol)
+
+# "auto"/"iterative": local systems above this dimension are solved by
+# warm-started GMRES on the structured operator (no dense matrix); at and
+# below it the dense device LU is cheaper than a few dozen GMRES iterations.
+_ITERATIVE_MIN_DIM = 8192
+_GMRES_RESTART = 40
+_GMRES_MAXIT = 400
+# beyond this dimension a dense fallback would not fit comfortably
+_DENSE_FALLBACK_MAX = 60000
+
+
+def _local_matvec(phi_l, a_p, phi_r, x):
+    """M x for the local operator M[(x,i,g),(y,j,h)] = sum_ab phi_l[x,a,y]
+    A[a,i,j,b] phi_r[g,b,h] (solver.py:136-139): three DMMA GEMMs."""
+    return _proj_a(phi_l, x, a_p, phi_r)
+
+
+def _gmres(mv, b, x0, rtol, restart=_GMRES_RESTART, maxit=_GMRES_MAXIT):
+    """Restarted GMRES (solver.py:186-195 uses scipy's, restart 40) on the
+    device: Arnoldi vectors, the matvec and the classical Gram-Schmidt
+    passes (twice, for orthogonality) run as device GEMMs; only the
+    (j+1)-vector of Hessenberg coefficients reaches the host per iteration,
+    where the Givens rotations live.  Returns (x, converged, iterations)."""
+    shape = b.shape
+    bv = b.reshape(-1)
+    dim = bv.numel()
+    bn = float(torch.linalg.vector_norm(bv))
+    if bn == 0.0:
+        return torch.zeros_like(b), True, 0
+    x = x0.reshape(-1).clone()
+    total = 0
+    V = torch.empty((restart + 1, dim), dtype=torch.float64, device=b.device)
+    while True:
+        r = bv - mv(x.view(shape)).reshape(-1)
+        beta = float(torch.linalg.vector_norm(r))
+        if beta <= rtol * bn:
+            return x.view(shape), True, total
+        if total >= maxit:
+            return x.view(shape), False, total
+        torch.div(r, beta, out=V[0])
+        H = np.zeros((restart + 1, restart))
+        cs = np.zeros(restart)
+        sn = np.zeros(restart)
+        g = np.zeros(restart + 1)
+        g[0] = beta
+        j_end = 0
+        for j in range(restart):
+            w = mv(V[j].view(shape)).reshape(-1, 1)
+            Vj = V[: j + 1]
+            h = mm(Vj, w)  # (j+1, 1)
+            w = mm(Vj, h, ta=True, out=w, alpha=-1.0, beta=1.0)
+            h2 = mm(Vj, w)
+            w = mm(Vj, h2, ta=True, out=w, alpha=-1.0, beta=1.0)
+            hn = torch.linalg.vector_norm(w)
+            hv = torch.cat([(h + h2).view(-1), hn.view(1)]).cpu().numpy()
+            H[: j + 2, j] = hv
+            if hv[-1] > 0.0:
+                torch.div(w.view(-1), hv[-1], out=V[j + 1])
+            for i in range(j):
+                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+                H[i, j] = t
+            den = np.hypot(H[j, j], H[j + 1, j])
+            cs[j], sn[j] = (1.0, 0.0) if den == 0.0 else (H[j, j] / den, H[j + 1, j] / den)
+            H[j, j] = den
+            H[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            total += 1
+            j_end = j + 1
+            if abs(g[j + 1]) <= rtol * bn or total >= maxit or hv[-1] == 0.0:
+                break
+        y = np.zeros(j_end)
+        for i in range(j_end - 1, -1, -1):
+            y[i] = (g[i] - H[i, i + 1:j_end] @ y[i + 1:]) / H[i, i]
+        yd = torch.from_numpy(y).to(b.device).view(-1, 1)
+        mm(V[:j_end], yd, ta=True, out=x.view(-1, 1), beta=1.0)
+
+
+def _solve_local(phi_l, a_p, phi_r, rhs, keep=False, x_cur=None, cfg=None, rtol=1e-12):
+    """Local system M x = rhs (solver.py:162-196).  ``direct``: dense device
+    LU (+ refinement / QR fallback).  ``iterative``/``auto`` above
+    _ITERATIVE_MIN_DIM: GMRES warm-started from the current core, with the
+    reference's local tolerance; a dense solve is the fallback when GMRES
+    does not converge.  With ``keep`` also returns the dense operator (None
+    on the iterative path)."""
     rl, n, rr = rhs.shape
     dim = rl * n * rr
+    iterative = cfg is not None and cfg.local_solver != "direct" and dim > _ITERATIVE_MIN_DIM
+    if iterative:
+        x0 = x_cur if (x_cur is not None and tuple(x_cur.shape) == tuple(rhs.shape)) else torch.zeros_like(rhs)
+        with _phase("local_gmres"):
+            sol, ok, its = _gmres(lambda v: _local_matvec(phi_l, a_p, phi_r, v), rhs, x0, rtol)
+        if PROFILE is not None:
+            PROFILE["gmres_its"] = PROFILE.get("gmres_its", 0) + its
+        if ok or dim > _DENSE_FALLBACK_MAX:
+            if _LOCAL_HOOK is not None:
+                _LOCAL_HOOK(phi_l, a_p, phi_r, rhs, x_cur, sol)
+            return (sol, None) if keep else sol
+        if PROFILE is not None:
+            PROFILE["gmres_fallbacks"] = PROFILE.get("gmres_fallbacks", 0) + 1
     if dim > _RELEASE_DIM:
         # local systems grow sweep by sweep; stale blocks of either cache
         # would otherwise pin tens of GB (see _lib.release_cached)
@@ -213,6 +315,8 @@ def _solve_local(phi_l, a_p, phi_r, rhs, keep=False):
         mcm = _local_matrix_cm(phi_l, a_p, phi_r)
     with _phase("local_lu"):
         sol, _ = dense_solve_colmajor(mcm, dim, rhs.reshape(-1))
+    if _LOCAL_HOOK is not None:
+        _LOCAL_HOOK(phi_l, a_p, phi_r, rhs, x_cur, sol.view(rl, n, rr))
     if keep:
         return sol.view(rl, n, rr), mcm
     return sol.view(rl, n, rr)
@@ -260,6 +364,32 @@ def _truncated_split_right(core, delta, rmax):
     vr = v[: (n * rr) * r].view(r, n, rr)  # V[:, :r] column-major == C-order (r, n, rr)
     carry = mm(core.reshape(rl, n * rr), vr.reshape(r, n * rr), tb=True)  # M V_r = U_r s_r
     return vr.contiguous(), carry
+
+
+def _residual_split_right_structured(core, phi_l, a_p, phi_r, rhs, tol, rmax):
+    """_residual_split_right without a dense operator: bisection on r with
+    structured local matvecs (the residual of x_r is non-increasing in r up
+    to rounding)."""
+    rl, n, rr = core.shape
+    s, v, k = svd_left_colmajor(core.contiguous().view(-1), n * rr, rl)
+    vk = v.view(k, n * rr)
+    carry_all = mm(core.reshape(rl, n * rr), vk, tb=True)  # (rl, k) = U S
+    bn = float(torch.linalg.vector_norm(rhs))
+
+    def res(r):
+        xr = mm(carry_all[:, :r].contiguous(), vk[:r].contiguous()).view(rl, n, rr)
+        return float(torch.linalg.vector_norm(_local_matvec(phi_l, a_p, phi_r, xr) - rhs))
+
+    target = max(tol * bn, 2.0 * res(k))
+    lo, hi = 1, k  # res(hi) <= target
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if res(mid) <= target:
+            hi = mid
+        else:
+            lo = mid + 1
+    r = max(1, min(hi, rmax))
+    return vk[:r].contiguous().view(r, n, rr), carry_all[:, :r].contiguous()
 
 
 def _residual_split_right(core, mcm, rhs, tol, rmax):
@@ -378,10 +508,11 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig, x0: TTVector | None = Non
     tol_loc = cfg.trunc_factor * cfg.epsilon / np.sqrt(d)
     sweeps_done = 0
     for sweep in range(cfg.max_sweeps):
+        rtol_local = max(0.02 * cfg.epsilon * adapt, 1e-13)  # solver.py:296
         # ---------------- forward: solve + enrich ----------------
         for k in range(d):
             rhs = _local_rhs(psi_l[k], F[k], psi_r[k + 1])
-            xk = _solve_local(phi_l[k], A[k], phi_r[k + 1], rhs)
+            xk = _solve_local(phi_l[k], A[k], phi_r[k + 1], rhs, x_cur=x[k], cfg=cfg, rtol=rtol_local)
             x[k] = xk
             if k < d - 1:
                 zrhs = _local_rhs(zf_l[k], F[k], zf_r[k + 1])
@@ -405,10 +536,14 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig, x0: TTVector | None = Non
         delta = cfg.trunc_factor * cfg.epsilon * adapt * max(xnorm, 1e-300) / np.sqrt(d)
         for k in range(d - 1, -1, -1):
             rhs = _local_rhs(psi_l[k], F[k], psi_r[k + 1])
-            xk, mcm = _solve_local(phi_l[k], A[k], phi_r[k + 1], rhs, keep=True)
+            xk, mcm = _solve_local(phi_l[k], A[k], phi_r[k + 1], rhs, keep=True, x_cur=x[k], cfg=cfg,
+                                   rtol=rtol_local)
             if k > 0:
                 with _phase("svd_split"):
-                    if residual_rule:
+                    if residual_rule and mcm is None:
+                        x[k], carry = _residual_split_right_structured(xk, phi_l[k], A[k], phi_r[k + 1], rhs,
+                                                                      tol_loc, cfg.max_rank)
+                    elif residual_rule:
                         x[k], carry = _residual_split_right(xk, mcm, rhs, tol_loc, cfg.max_rank)
                     else:
                         x[k], carry = _truncated_split_right(xk, delta, cfg.max_rank)

@@ -148,3 +148,25 @@ def test_tt_ops_golden():
         assert abs(T.tt_dot(tx, ty) - g[f"{name}_dot"]) <= 1e-12 * T.tt_norm(tx) * T.tt_norm(ty)
     out = S.apply_tt_matrix(T.TTMatrix(cases.apply_case()), g["apply_v"])
     assert rel(out.cpu().numpy(), g["apply_out"]) < 1e-13
+
+
+@pytest.mark.parametrize("d", [3, 4])
+def test_variable_modulus_assembly_matches_oracle(d):
+    """Config-4 extension (E(x,y) at the Gauss points): device assembly vs the
+    oracle restatement (itself pinned by tests/test_oracle_config4.py)."""
+    from oracle import fem as F
+    from oracle import tt as O
+    from paper_2501_07778_b200 import assembly as A
+    from paper_2501_07778_b200.material import MaterialModel, config4_modulus
+    from paper_2501_07778_b200.mesh import SubdomainMesh
+    from paper_2501_07778_b200.ttcore import tt_contract
+
+    unit = np.array([[0.0, 0.0], [1.0, 0.0], [1.0, 1.0], [0.0, 1.0]])
+    mat = MaterialModel(1.0, 0.3, "plane-stress", modulus_field=config4_modulus)
+    mesh = SubdomainMesh(unit, d, {"left": "clamped"})
+    ref = F.assemble(mesh, mat, "zorder", 1e-10, body=(0.0, -1.0))
+    got = A.assemble_subdomain(mesh, mat, "zorder", 1e-10, body_force=(0.0, -1.0), cache=False)
+    for blk in ("kxx", "kxy", "kyx", "kyy", "fx", "fy"):
+        t = getattr(got, blk)
+        assert t.ranks == O.ranks(ref[blk]), (blk, t.ranks, O.ranks(ref[blk]))
+        assert rel(tt_contract(t), O.full(ref[blk])) < 1e-9, blk

@@ -63,6 +63,45 @@ def test_solve_matches_reference(name, truncation):
     assert np.linalg.norm(kd @ u_gpu - fd) / np.linalg.norm(fd) <= eps * (1 + 1e-6)
 
 
+@pytest.mark.parametrize("name", ["single3", "lshape2"])
+def test_iterative_local_solver_matches_direct(name, monkeypatch):
+    """local_solver="auto" with every local system on the device GMRES path
+    (threshold lowered) converges to the same solution as the dense path."""
+    from paper_2501_07778_b200 import solver as S
+    from paper_2501_07778_b200.ttcore import tt_contract
+
+    g = load("coupling")
+    gsys, spec = global_system(name)
+    eps = spec["solve"]
+    monkeypatch.setattr(S, "_ITERATIVE_MIN_DIM", 0)
+    prof = {}
+    monkeypatch.setattr(S, "PROFILE", prof)
+    out = S.solve(gsys.K, gsys.f, S.SolverConfig(epsilon=eps, seed=0, local_solver="auto",
+                                                 truncation="residual", enrichment_rank=8))
+    assert out.converged and out.residual <= eps
+    assert prof.get("gmres_its", 0) > 0
+    kd, fd = g[f"{name}_Kd"], g[f"{name}_fd"]
+    u = tt_contract(out.u)
+    assert np.linalg.norm(kd @ u - fd) / np.linalg.norm(fd) <= eps * (1 + 1e-6)
+    u_exact = np.linalg.solve(kd, fd)
+    assert np.linalg.norm(u - u_exact) / np.linalg.norm(u_exact) <= np.linalg.cond(kd) * eps + 1e-10
+
+
+def test_gmres_kernel_path():
+    """Device GMRES on a dense nonsymmetric system through the DMMA GEMMs."""
+    import torch
+
+    from paper_2501_07778_b200 import solver as S
+
+    rng = np.random.default_rng(5)
+    n = 500
+    m = torch.tensor(rng.standard_normal((n, n)) / np.sqrt(n) + 4 * np.eye(n), device="cuda")
+    b = torch.tensor(rng.standard_normal(n), device="cuda")
+    x, ok, its = S._gmres(lambda v: (m @ v.reshape(-1)).reshape(v.shape), b, torch.zeros_like(b), 1e-12)
+    assert ok and its < 100
+    assert float(torch.linalg.vector_norm(m @ x - b) / torch.linalg.vector_norm(b)) <= 1e-11
+
+
 def test_identity_solve_and_zero_rhs():
     from paper_2501_07778_b200 import solver as S
     from paper_2501_07778_b200 import ttcore as T
