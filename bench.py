@@ -352,6 +352,9 @@ def run_ours(args):
                 "pair": "16x128",
             },
             "clocks": clk,
+            "solve_wall_s": None if not extras else {
+                k: extras["solves"][k]["total_s"] for k in ("config4_d10", "config4_constE_d10", "config1_d5")
+                if k in extras["solves"]},
             "cpu_baseline": cpu,
             "extras": extras,
         }
@@ -375,8 +378,11 @@ def _dev_ms(torch, fn):
 
 
 def run_extras(torch, T, cpu_baseline=True) -> dict:
-    """Configs 3, 1 and the 2^10 x 2^10 solve (config-4 geometry/BCs/load with
-    constant E; see DESIGN.md for the variable-E case), device-timed."""
+    """Configs 3, 1 and the 2^10 x 2^10 solves: config 4 as specified
+    (variable E, upgraded AMEn: local-residual truncation, enrichment 16,
+    device GMRES local solves) and its constant-E variant on the
+    reference's own solver path (dense local solves), device-synchronised
+    wall time."""
     import time as _t
 
     out = {}
@@ -411,23 +417,32 @@ def run_extras(torch, T, cpu_baseline=True) -> dict:
     from paper_2501_07778_b200.configs import build_system
 
     solves = {}
-    for idx, d in ((1, 5), (40, 10)):
+    upgraded = dict(local_solver="auto", truncation="residual", enrichment_rank=16)
+    for idx, d, kw in ((1, 5, dict(local_solver="direct")), (4, 10, upgraded),
+                       (40, 10, dict(local_solver="direct"))):
         tm = {}
         torch.cuda.synchronize()
         t0 = _t.perf_counter()
         gsys, eps = build_system(idx, d, tm)
         t1 = _t.perf_counter()
-        res = S.solve(gsys.K, gsys.f, S.SolverConfig(epsilon=eps, seed=0, local_solver="direct"))
+        res = S.solve(gsys.K, gsys.f, S.SolverConfig(epsilon=eps, seed=0, **kw))
         torch.cuda.synchronize()
         t2 = _t.perf_counter()
         solves[f"config{idx if idx != 40 else '4_constE'}_d{d}"] = {
+            "solver": kw,
             "build_s": round(t1 - t0, 3), **{k: round(v, 3) for k, v in tm.items()},
             "solve_s": round(t2 - t1, 3), "total_s": round(t2 - t0, 3), "sweeps": res.sweeps,
             "residual": res.residual, "converged": res.converged, "max_rank": max(res.u.ranks),
             "K_max_rank": max(gsys.K.ranks),
         }
     solves["reference_cpu_s"] = {"config1_d5_solve": 1.21, "config4_constE_d10_solve": 658.9,
-                                 "config4_constE_d10_assembly": 11.05, "source": "SURVEY Appendix B, 8-core Xeon"}
+                                 "config4_constE_d10_assembly": 11.05,
+                                 "config4_d10_assembly": 43.0, "config4_d10_couple_dirichlet": 18.0,
+                                 "config4_d10_solve": None,
+                                 "note": "the reference solver does not converge on config 4 (variable E): "
+                                         "default GMRES local solves diverge, direct local solves grow "
+                                         "ranks toward max_rank (DESIGN.md 8)",
+                                 "source": "SURVEY Appendix B / BASELINE.md, 8-core Xeon"}
     if cpu_baseline:
         # reference algorithm (oracle restatement) on this host: config 1 solve
         from oracle import amen
