@@ -5,6 +5,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdlib>
+#include <string>
 
 #include "linalg.cuh"
 
@@ -497,6 +498,239 @@ size_t jacobi_cluster_smem(int px, int pw, int k, int cs) {
   return sizeof(double) * ((size_t)(px + pw) * kp + 3 * (size_t)kp * cs + kp + 16);
 }
 
+// Ring one-sided Jacobi (Brent-Luk ordering), the default for p + k <= 640.
+// A warp OWNS one column pair per round and holds both augmented columns
+// [X(:,c); W(:,c)] in registers (lane l keeps rows l, l+32, ...), so the
+// dots, the rotation decision and the rotation itself need no block-level
+// reduction.  After the rotation the two columns are pushed straight into
+// the (double-buffered, parity = round number) shared-memory slots of the
+// pairs that own them in the next round: in the circle schedule the column
+// at position pos moves to pos-1 (position 1 wraps to kp-1, 0 is fixed), so
+// side-0 columns go to pair q-1 and side-1 columns to pair q+1, which is the
+// same CTA except at the chunk edges (those stores cross DSMEM).  One cluster
+// barrier per round and no partial-sum traffic; after a whole sweep
+// (kp-1 rounds) every column is back at its starting position, so the
+// output needs no permutation.  Convergence is agreed by pushing a per-sweep
+// "rotated" flag to every CTA before the sweep's last barrier.
+constexpr int JR_MAXL = 640;  // p + k limit (E = 20 registers-pairs per lane)
+
+__device__ __forceinline__ void ring_dest(int q, int side, int np, int& dq, int& dside) {
+  if (np == 1) {
+    dq = 0;
+    dside = side;
+  } else if (side == 0) {
+    dq = q <= 1 ? 0 : q - 1;
+    dside = q == 1 ? 1 : 0;
+  } else {
+    dq = q == np - 1 ? q : q + 1;
+    dside = q == np - 1 ? 0 : 1;
+  }
+}
+
+template <int E, int MAXT>
+__global__ void __launch_bounds__(MAXT) jacobi_ring_kernel(int p, int k, double* X, int64_t ldx,
+                                                           double* W, int64_t ldw, double tol,
+                                                           int ppc) {
+  extern __shared__ double jr[];  // [2 parity][ppc][2 side][32 E]
+  __shared__ double nrm[16];
+  __shared__ int anyrot[2];
+  constexpr int LP = 32 * E;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cs = (int)cluster.num_blocks();
+  const int cr = (int)cluster.block_rank();
+  const int kp = k + (k & 1), np = kp / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = cr * ppc + warp;
+  const bool active = q < np;
+  const int c0 = q, c1 = kp - 1 - q;  // columns at round 0 (and after every sweep)
+  double u[E], v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int t = lane + 32 * e;
+    double a = 0.0, b = 0.0;
+    if (active) {
+      if (t < p) {
+        a = X[t + (int64_t)c0 * ldx];
+        b = c1 < k ? X[t + (int64_t)c1 * ldx] : 0.0;
+      } else if (t < p + k) {
+        a = (t - p == c0) ? 1.0 : 0.0;
+        b = (t - p == c1 && c1 < k) ? 1.0 : 0.0;
+      }
+    }
+    u[e] = a;
+    v[e] = b;
+  }
+  if (threadIdx.x < 2) anyrot[threadIdx.x] = 0;
+  {
+    double acc = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (lane + 32 * e < p) acc = fma(u[e], u[e], fma(v[e], v[e], acc));
+    acc = warp_sum(acc);
+    __shared__ double red[32];
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if ((int)threadIdx.x < cs) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+      cluster.map_shared_rank(nrm, (int)threadIdx.x)[cr] = t;
+    }
+  }
+  cluster.sync();
+  double noise2 = 0.0;
+  for (int c = 0; c < cs; ++c) noise2 += nrm[c];
+  noise2 *= kEps * kEps;
+  const double tol2 = tol * tol;
+
+  int dq0, ds0, dq1, ds1;
+  ring_dest(q, 0, np, dq0, ds0);
+  ring_dest(q, 1, np, dq1, ds1);
+  // local stores stay st.shared; only chunk-edge columns cross DSMEM
+  double* const base0 = dq0 / ppc == cr ? jr : cluster.map_shared_rank(jr, dq0 / ppc);
+  double* const base1 = dq1 / ppc == cr ? jr : cluster.map_shared_rank(jr, dq1 / ppc);
+  double* const dst0 = base0 + ((size_t)(dq0 % ppc) * 2 + ds0) * LP;
+  double* const dst1 = base1 + ((size_t)(dq1 % ppc) * 2 + ds1) * LP;
+  const size_t parity_stride = (size_t)ppc * 2 * LP;
+  double* const mine = jr + (size_t)warp * 2 * LP;
+
+  int sweep = 0, rn = 0;
+  for (; sweep < JMAXSWEEPS; ++sweep) {
+    int rotated = 0;
+    for (int r = 0; r < kp - 1; ++r, ++rn) {
+      const size_t par = (size_t)(rn & 1) * parity_stride;
+      if (active) {
+        double a = 0.0, b = 0.0, g = 0.0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          if (lane + 32 * e < p) {
+            a = fma(u[e], u[e], a);
+            b = fma(v[e], v[e], b);
+            g = fma(u[e], v[e], g);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          g += __shfl_xor_sync(0xffffffffu, g, o);
+        }
+        // same decision and rotation as jacobi_pair; the divisions and
+        // square roots go through the Newton-refined hardware approximations
+        // (the round's critical path is this scalar chain).
+        if (g != 0.0 && a >= noise2 && b >= noise2 && g * g > tol2 * a * b) {
+          const double zeta = (b - a) * rcp_nr(2.0 * g);
+          const double az = fabs(zeta);
+          double t;
+          if (az < 1e100) {
+            const double w = fma(zeta, zeta, 1.0);
+            t = rcp_nr(az + w * rsqrt_nr(w));
+          } else {
+            t = 0.5 * rcp_nr(az);
+          }
+          t = zeta >= 0.0 ? t : -t;
+          const double c = rsqrt_nr(fma(t, t, 1.0));
+          const double sn = c * t;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const double x = u[e], y = v[e];
+            u[e] = c * x - sn * y;
+            v[e] = sn * x + c * y;
+          }
+          rotated = 1;
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          dst0[par + lane + 32 * e] = u[e];
+          dst1[par + lane + 32 * e] = v[e];
+        }
+        if (r == kp - 2 && rotated && lane < cs)
+          (lane == cr ? anyrot : cluster.map_shared_rank(anyrot, lane))[sweep & 1] = 1;
+      }
+      if (cs == 1) __syncthreads();
+      else cluster.sync();
+      if (active) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          u[e] = mine[par + lane + 32 * e];
+          v[e] = mine[par + LP + lane + 32 * e];
+        }
+      }
+    }
+    const int more = anyrot[sweep & 1];
+    __syncthreads();
+    if (threadIdx.x == 0) anyrot[sweep & 1] = 0;
+    if (!more) break;
+  }
+  if (cr == 0 && threadIdx.x == 0) g_jacobi_sweeps = min(sweep + 1, JMAXSWEEPS);
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int t = lane + 32 * e;
+      if (t < p) {
+        X[t + (int64_t)c0 * ldx] = u[e];
+        if (c1 < k) X[t + (int64_t)c1 * ldx] = v[e];
+      } else if (t < p + k) {
+        W[(t - p) + (int64_t)c0 * ldw] = u[e];
+        if (c1 < k) W[(t - p) + (int64_t)c1 * ldw] = v[e];
+      }
+    }
+  }
+  cluster.sync();  // no CTA exits while a neighbour may still push into it
+}
+
+template <int E, int MAXT>
+int launch_ring_t(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw,
+                  double tol, int cs, int ppc, size_t smem) {
+  static bool configured = false;
+  if (!configured) {
+    QTT_CUDA(cudaFuncSetAttribute(jacobi_ring_kernel<E, MAXT>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+    QTT_CUDA(cudaFuncSetAttribute(jacobi_ring_kernel<E, MAXT>,
+                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs, 1, 1);
+  cfg.blockDim = dim3(ppc * 32, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  QTT_CUDA(cudaLaunchKernelEx(&cfg, jacobi_ring_kernel<E, MAXT>, p, k, X, ldx, W, ldw, tol, ppc));
+  note_launch();
+  return kOk;
+}
+
+// Returns kUnsupported when the problem does not fit the ring kernel.
+int jacobi_ring(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw,
+                double tol) {
+  const int L = p + k;
+  if (L > JR_MAXL || k < 1) return kUnsupported;
+  const int E = (int)ceil_div(L, 32);
+  const int Et = E <= 4 ? 4 : E <= 8 ? 8 : E <= 12 ? 12 : E <= 16 ? 16 : 20;
+  const int maxw = Et <= 8 ? 32 : 16;  // register budget: 1024 threads need <= 64 regs
+  const int np = (k + (k & 1)) / 2;
+  for (int cs = 1; cs <= 16; ++cs) {
+    const int ppc = (int)ceil_div(np, cs);
+    const size_t smem = sizeof(double) * 4 * (size_t)ppc * 32 * Et;
+    if (ppc > maxw || smem > 210 * 1024) continue;
+    if (ceil_div(np, ppc) != cs) continue;  // every CTA of the cluster owns >= 1 pair
+    switch (Et) {
+      case 4: return launch_ring_t<4, 1024>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem);
+      case 8: return launch_ring_t<8, 1024>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem);
+      case 12: return launch_ring_t<12, 512>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem);
+      case 16: return launch_ring_t<16, 512>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem);
+      default: return launch_ring_t<20, 512>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem);
+    }
+  }
+  return kUnsupported;
+}
+
 // Large problems: cooperative grid, columns stay in global memory (L2).
 __global__ void __launch_bounds__(256) jacobi_grid_kernel(int p, int k, double* X, int64_t ldx,
                                                           double* W, int64_t ldw, double tol,
@@ -812,6 +1046,13 @@ static int jacobi_impl(cudaStream_t s, int p, int k, double* X, int64_t ldx, dou
   // rounding noise: singular values move at second order (~1e-28) and the
   // singular vectors stay orthogonal to ~1e-14.
   const double tol = 32.0 * sqrt((double)std::max(p, 1)) * kEps;
+  // QTT_JACOBI_KERNEL=legacy forces the row-distributed kernels (A/B checks).
+  static const char* kern = getenv("QTT_JACOBI_KERNEL");
+  static const bool legacy = kern && std::string(kern) == "legacy";
+  if (!legacy) {
+    const int st = jacobi_ring(s, p, k, X, ldx, W, ldw, tol);
+    if (st != kUnsupported) return st;
+  }
   const size_t smem = sizeof(double) * ((size_t)p * k + (size_t)k * k);
   if (smem <= 200 * 1024) {
     static bool configured = false;
