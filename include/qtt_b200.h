@@ -171,6 +171,26 @@ int qtt_element_grids(int32_t d, int32_t zorder, int32_t ngauss,
 int qtt_dense_solve(int64_t n, const double* m, int64_t ldm, const double* b,
                     double* x, int32_t* fallback, void* stream);
 
+/* Restarted GMRES on the structured AMEn local operator, replaces the
+ * scipy.sparse.linalg.gmres call of solver._solve_local (solver.py:186-195:
+ * restart, rtol, atol = 0, warm start x0).  The operator
+ *   M[(x,i,g),(y,j,h)] = sum_ab phi_l[x,a,y] A[a,i,j,b] phi_r[g,b,h]
+ * is applied without being formed (solver._proj_a): phi_l (rl,ra,rl),
+ * a_jib = A permuted to (a,j,i,b) as a row-major (ra*n) x (n*rb) matrix,
+ * phi_r (rr,rb,rr), rhs/x0/x (rl,n,rr), all C-order on the device (x may
+ * alias x0).  abort_early != 0 stops once the first cycles' rate projects
+ * past maxit (the caller then solves densely).  *iters / *converged report
+ * the outcome; non-convergence is not an error. */
+int qtt_local_gmres(int64_t rl, int64_t n, int64_t rr, int64_t ra, int64_t rb,
+                    const double* phi_l, const double* a_jib, const double* phi_r,
+                    const double* rhs, const double* x0, double* x, double rtol,
+                    int32_t restart, int32_t maxit, int32_t abort_early,
+                    int32_t* iters, int32_t* converged, void* stream);
+/* y = M x for the same operator (solver._local_matvec, solver.py:136-139). */
+int qtt_local_apply(int64_t rl, int64_t n, int64_t rr, int64_t ra, int64_t rb,
+                    const double* phi_l, const double* a_jib, const double* phi_r,
+                    const double* x, double* y, void* stream);
+
 /* ------------------------------------------------------ dense primitives
  * Exposed for the parity tests of the building blocks. */
 int qtt_gemm(int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,

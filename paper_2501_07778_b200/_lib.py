@@ -46,6 +46,8 @@ EXPORTS = (
     "qtt_z_index",
     "qtt_element_grids",
     "qtt_dense_solve",
+    "qtt_local_gmres",
+    "qtt_local_apply",
     "qtt_gemm",
     "qtt_qr",
     "qtt_svd",

@@ -128,6 +128,22 @@ int contract(const qtt_layout* L, const double* a, double* dense, cudaStream_t s
   return kOk;
 }
 
+// core (r0, n, m, r1) C-order -> out[i][(j*r0 + q) * r1 + p] = core[q, i, j, p]
+__global__ void repack_core_kernel(int r0, int n, int m, int r1, const double* __restrict__ core,
+                                   double* __restrict__ out) {
+  const int64_t total = (int64_t)r0 * n * m * r1;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int p = (int)(t % r1);
+    int64_t rest = t / r1;
+    const int q = (int)(rest % r0);
+    rest /= r0;
+    const int j = (int)(rest % m);
+    const int i = (int)(rest / m);
+    out[t] = core[(((int64_t)q * n + i) * m + j) * r1 + p];
+  }
+}
+
 // y = A v for a dense v (solver.apply_tt_matrix, solver.py:57-73).  The
 // running tensor T_k is column-major (r_k*m_k x L_k) with rows (bond, col
 // bit) and the finished row bits appended as the slowest axes.
@@ -148,9 +164,13 @@ int dense_apply(const qtt_layout* LA, const double* a, const double* v, double* 
       maxbuf = std::max(maxbuf, LA->ranks[l + 1] * rem_cols * done_rows);
     }
   }
-  double *b0, *b1;
+  int64_t maxcore = 1;
+  for (int l = 0; l < d; ++l)
+    maxcore = std::max(maxcore, LA->ranks[l] * LA->rows[l] * LA->cols[l] * LA->ranks[l + 1]);
+  double *b0, *b1, *apk;
   QTT_CUDA(cudaMallocAsync(&b0, sizeof(double) * maxbuf, s));
   QTT_CUDA(cudaMallocAsync(&b1, sizeof(double) * maxbuf, s));
+  QTT_CUDA(cudaMallocAsync(&apk, sizeof(double) * maxcore, s));
   QTT_CUDA(cudaMemcpyAsync(b0, v, sizeof(double) * cols, cudaMemcpyDeviceToDevice, s));
   double* cur = b0;
   double* nxt = b1;
@@ -162,20 +182,21 @@ int dense_apply(const qtt_layout* LA, const double* a, const double* v, double* 
     const int64_t Lc = rem_cols * done_rows;  // columns of T_k viewed (r0*m x Lc)
     if (Lc > 0x7fffffff) return kUnsupported;
     const double* core = a + LA->offsets[l];
-    for (int i = 0; i < n; ++i) {
-      for (int j = 0; j < m; ++j) {
-        // T_{k+1}[:, block i] (+)= A_{i,j}^T (r1 x r0) * T_k[rows r0*j .. , :]
-        QTT_TRY(dgemm(s, 0, 0, r1, (int)Lc, r0, 1.0, core + (int64_t)(i * m + j) * r1,
-                      (int64_t)n * m * r1, cur + (int64_t)r0 * j, (int64_t)r0 * m,
-                      j == 0 ? 0.0 : 1.0, nxt + (int64_t)r1 * Lc * i, r1));
-      }
-    }
+    // Repack the core so that, per row bit i, A_i (r1 x m*r0) has column
+    // index j*r0 + q matching T_k's row order: one K = m*r0 GEMM per i
+    // instead of m accumulating K = r0 GEMMs (T_{k+1} written once).
+    repack_core_kernel<<<grid1d((int64_t)r0 * n * m * r1), 256, 0, s>>>(r0, n, m, r1, core, apk);
+    QTT_CHECK_LAUNCH();
+    for (int i = 0; i < n; ++i)
+      QTT_TRY(dgemm(s, 0, 0, r1, (int)Lc, m * r0, 1.0, apk + (int64_t)i * r1 * m * r0, r1, cur,
+                    (int64_t)r0 * m, 0.0, nxt + (int64_t)r1 * Lc * i, r1));
     done_rows *= n;
     std::swap(cur, nxt);
   }
   QTT_CUDA(cudaMemcpyAsync(out, cur, sizeof(double) * rows, cudaMemcpyDeviceToDevice, s));
   QTT_CUDA(cudaFreeAsync(b0, s));
   QTT_CUDA(cudaFreeAsync(b1, s));
+  QTT_CUDA(cudaFreeAsync(apk, s));
   return kOk;
 }
 

@@ -39,7 +39,7 @@ from .ttcore import (
 
 __all__ = ["SolverConfig", "SolveOutcome", "solve", "residual", "apply_tt_matrix"]
 
-_RELEASE_DIM = 12000  # local systems above ~1.1 GB trim the allocator caches first
+_RELEASE_DIM = 30000  # local systems above ~7 GB trim the allocator caches first
 _DENSE_LOCAL_LIMIT = 1200  # kept for API parity (solver.py:23); local solves are direct
 
 _TRACE = bool(__import__("os").environ.get("QTT_AMEN_TRACE"))
@@ -219,70 +219,34 @@ _DENSE_FALLBACK_MAX = 60000
 
 def _local_matvec(phi_l, a_p, phi_r, x):
     """M x for the local operator M[(x,i,g),(y,j,h)] = sum_ab phi_l[x,a,y]
-    A[a,i,j,b] phi_r[g,b,h] (solver.py:136-139): three DMMA GEMMs."""
-    return _proj_a(phi_l, x, a_p, phi_r)
+    A[a,i,j,b] phi_r[g,b,h] (solver.py:136-139): qtt_local_apply (three DMMA
+    GEMMs and two permutations, one C-ABI call)."""
+    rl, n, rr = x.shape
+    y = torch.empty_like(x)
+    _lib.call("qtt_local_apply", ctypes.c_int64(rl), ctypes.c_int64(n), ctypes.c_int64(rr),
+              ctypes.c_int64(a_p["ra"]), ctypes.c_int64(a_p["rb"]), _lib.ptr(phi_l.contiguous()),
+              _lib.ptr(a_p["aj_ib"]), _lib.ptr(phi_r.contiguous()), _lib.ptr(x.contiguous()),
+              _lib.ptr(y), _lib.stream_handle())
+    return y
 
 
-def _gmres(mv, b, x0, rtol, restart=_GMRES_RESTART, maxit=_GMRES_MAXIT):
+def _gmres(phi_l, a_p, phi_r, b, x0, rtol, restart=_GMRES_RESTART, maxit=_GMRES_MAXIT,
+           abort_early=False):
     """Restarted GMRES (solver.py:186-195 uses scipy's, restart 40) on the
-    device: Arnoldi vectors, the matvec and the classical Gram-Schmidt
-    passes (twice, for orthogonality) run as device GEMMs; only the
-    (j+1)-vector of Hessenberg coefficients reaches the host per iteration,
-    where the Givens rotations live.  Returns (x, converged, iterations)."""
-    shape = b.shape
-    bv = b.reshape(-1)
-    dim = bv.numel()
-    bn = float(torch.linalg.vector_norm(bv))
-    if bn == 0.0:
-        return torch.zeros_like(b), True, 0
-    x = x0.reshape(-1).clone()
-    total = 0
-    V = torch.empty((restart + 1, dim), dtype=torch.float64, device=b.device)
-    while True:
-        r = bv - mv(x.view(shape)).reshape(-1)
-        beta = float(torch.linalg.vector_norm(r))
-        if beta <= rtol * bn:
-            return x.view(shape), True, total
-        if total >= maxit:
-            return x.view(shape), False, total
-        torch.div(r, beta, out=V[0])
-        H = np.zeros((restart + 1, restart))
-        cs = np.zeros(restart)
-        sn = np.zeros(restart)
-        g = np.zeros(restart + 1)
-        g[0] = beta
-        j_end = 0
-        for j in range(restart):
-            w = mv(V[j].view(shape)).reshape(-1, 1)
-            Vj = V[: j + 1]
-            h = mm(Vj, w)  # (j+1, 1)
-            w = mm(Vj, h, ta=True, out=w, alpha=-1.0, beta=1.0)
-            h2 = mm(Vj, w)
-            w = mm(Vj, h2, ta=True, out=w, alpha=-1.0, beta=1.0)
-            hn = torch.linalg.vector_norm(w)
-            hv = torch.cat([(h + h2).view(-1), hn.view(1)]).cpu().numpy()
-            H[: j + 2, j] = hv
-            if hv[-1] > 0.0:
-                torch.div(w.view(-1), hv[-1], out=V[j + 1])
-            for i in range(j):
-                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
-                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
-                H[i, j] = t
-            den = np.hypot(H[j, j], H[j + 1, j])
-            cs[j], sn[j] = (1.0, 0.0) if den == 0.0 else (H[j, j] / den, H[j + 1, j] / den)
-            H[j, j] = den
-            H[j + 1, j] = 0.0
-            g[j + 1] = -sn[j] * g[j]
-            g[j] = cs[j] * g[j]
-            total += 1
-            j_end = j + 1
-            if abs(g[j + 1]) <= rtol * bn or total >= maxit or hv[-1] == 0.0:
-                break
-        y = np.zeros(j_end)
-        for i in range(j_end - 1, -1, -1):
-            y[i] = (g[i] - H[i, i + 1:j_end] @ y[i + 1:]) / H[i, i]
-        yd = torch.from_numpy(y).to(b.device).view(-1, 1)
-        mm(V[:j_end], yd, ta=True, out=x.view(-1, 1), beta=1.0)
+    structured local operator: qtt_local_gmres runs the whole iteration on
+    the device, driven from C++ (CGS2 Arnoldi, host Givens).  Returns
+    (x, converged, iterations)."""
+    rl, n, rr = b.shape
+    x = x0.contiguous().clone()
+    its = ctypes.c_int32(0)
+    conv = ctypes.c_int32(0)
+    _lib.call("qtt_local_gmres", ctypes.c_int64(rl), ctypes.c_int64(n), ctypes.c_int64(rr),
+              ctypes.c_int64(a_p["ra"]), ctypes.c_int64(a_p["rb"]), _lib.ptr(phi_l.contiguous()),
+              _lib.ptr(a_p["aj_ib"]), _lib.ptr(phi_r.contiguous()), _lib.ptr(b.contiguous()),
+              _lib.ptr(x), _lib.ptr(x), ctypes.c_double(rtol), ctypes.c_int32(restart),
+              ctypes.c_int32(maxit), ctypes.c_int32(1 if abort_early else 0), ctypes.byref(its),
+              ctypes.byref(conv), _lib.stream_handle())
+    return x, bool(conv.value), int(its.value)
 
 
 def _solve_local(phi_l, a_p, phi_r, rhs, keep=False, x_cur=None, cfg=None, rtol=1e-12):
@@ -297,10 +261,13 @@ def _solve_local(phi_l, a_p, phi_r, rhs, keep=False, x_cur=None, cfg=None, rtol=
     iterative = cfg is not None and cfg.local_solver != "direct" and dim > _ITERATIVE_MIN_DIM
     if iterative:
         x0 = x_cur if (x_cur is not None and tuple(x_cur.shape) == tuple(rhs.shape)) else torch.zeros_like(rhs)
+        tg = PROFILE.get("local_gmres", 0.0) if PROFILE is not None else 0.0
         with _phase("local_gmres"):
-            sol, ok, its = _gmres(lambda v: _local_matvec(phi_l, a_p, phi_r, v), rhs, x0, rtol)
+            sol, ok, its = _gmres(phi_l, a_p, phi_r, rhs, x0, rtol, abort_early=dim <= _DENSE_FALLBACK_MAX)
         if PROFILE is not None:
             PROFILE["gmres_its"] = PROFILE.get("gmres_its", 0) + its
+            PROFILE.setdefault("calls", []).append(
+                ("gmres", rl, a_p["ra"], rr, its, bool(ok), round(PROFILE["local_gmres"] - tg, 4)))
         if ok or dim > _DENSE_FALLBACK_MAX:
             if _LOCAL_HOOK is not None:
                 _LOCAL_HOOK(phi_l, a_p, phi_r, rhs, x_cur, sol)
@@ -313,8 +280,12 @@ def _solve_local(phi_l, a_p, phi_r, rhs, keep=False, x_cur=None, cfg=None, rtol=
         _lib.release_cached()
     with _phase("local_matrix"):
         mcm = _local_matrix_cm(phi_l, a_p, phi_r)
+    tl = PROFILE.get("local_lu", 0.0) if PROFILE is not None else 0.0
     with _phase("local_lu"):
         sol, _ = dense_solve_colmajor(mcm, dim, rhs.reshape(-1))
+    if PROFILE is not None:
+        PROFILE.setdefault("calls", []).append(
+            ("lu", rl, a_p["ra"], rr, dim, True, round(PROFILE["local_lu"] - tl, 4)))
     if _LOCAL_HOOK is not None:
         _LOCAL_HOOK(phi_l, a_p, phi_r, rhs, x_cur, sol.view(rl, n, rr))
     if keep:
@@ -524,13 +495,15 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig, x0: TTVector | None = Non
                 nxt = x[k + 1]
                 nxt = torch.cat([nxt, torch.zeros((w.shape[2],) + tuple(nxt.shape[1:]), dtype=torch.float64,
                                                   device=dev)], dim=0)
-                x[k], carry = _qr_core_left(xe)
+                with _phase("enrich_qr"):
+                    x[k], carry = _qr_core_left(xe)
                 r0, n1, r2 = nxt.shape
                 x[k + 1] = mm(carry, nxt.reshape(r0, n1 * r2)).view(carry.shape[0], n1, r2)
-                phi_l[k + 1] = _phi_left(phi_l[k], x[k], A[k], x[k])
-                psi_l[k + 1] = _psi_left(psi_l[k], x[k], F[k])
-                za_l[k + 1] = _phi_left(za_l[k], z[k], A[k], x[k])
-                zf_l[k + 1] = _psi_left(zf_l[k], z[k], F[k])
+                with _phase("env"):
+                    phi_l[k + 1] = _phi_left(phi_l[k], x[k], A[k], x[k])
+                    psi_l[k + 1] = _psi_left(psi_l[k], x[k], F[k])
+                    za_l[k + 1] = _phi_left(za_l[k], z[k], A[k], x[k])
+                    zf_l[k + 1] = _psi_left(zf_l[k], z[k], F[k])
         # ---------------- backward: solve + truncate ----------------
         xnorm = float(torch.linalg.vector_norm(x[d - 1]))
         delta = cfg.trunc_factor * cfg.epsilon * adapt * max(xnorm, 1e-300) / np.sqrt(d)
@@ -550,11 +523,12 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig, x0: TTVector | None = Non
                 del mcm
                 p0, pn, p1 = x[k - 1].shape
                 x[k - 1] = mm(x[k - 1].reshape(p0 * pn, p1), carry).view(p0, pn, carry.shape[1])
-                phi_r[k] = _phi_right(phi_r[k + 1], x[k], A[k], x[k])
-                psi_r[k] = _psi_right(psi_r[k + 1], x[k], F[k])
-                z[k], _ = _qr_core_right(_safe_core(z[k], rng))
-                za_r[k] = _phi_right(za_r[k + 1], z[k], A[k], x[k])
-                zf_r[k] = _psi_right(zf_r[k + 1], z[k], F[k])
+                with _phase("env"):
+                    phi_r[k] = _phi_right(phi_r[k + 1], x[k], A[k], x[k])
+                    psi_r[k] = _psi_right(psi_r[k + 1], x[k], F[k])
+                    z[k], _ = _qr_core_right(_safe_core(z[k], rng))
+                    za_r[k] = _phi_right(za_r[k + 1], z[k], A[k], x[k])
+                    zf_r[k] = _psi_right(zf_r[k + 1], z[k], F[k])
             else:
                 x[k] = xk
         sweeps_done = sweep + 1

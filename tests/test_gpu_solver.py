@@ -87,19 +87,61 @@ def test_iterative_local_solver_matches_direct(name, monkeypatch):
     assert np.linalg.norm(u - u_exact) / np.linalg.norm(u_exact) <= np.linalg.cond(kd) * eps + 1e-10
 
 
-def test_gmres_kernel_path():
-    """Device GMRES on a dense nonsymmetric system through the DMMA GEMMs."""
+def _structured_local(rl, n, rr, ra, rb, seed, shift=4.0):
+    rng = np.random.default_rng(seed)
+    pl = rng.standard_normal((rl, ra, rl)) / rl
+    a = rng.standard_normal((ra, n, n, rb)) / n
+    pr = rng.standard_normal((rr, rb, rr)) / rr
+    pl[:, 0, :] = shift * np.eye(rl)
+    a[0, :, :, 0] = np.eye(n)
+    pr[:, 0, :] = np.eye(rr)
+    m = np.einsum("xay,aijb,gbh->xigyjh", pl, a, pr).reshape(rl * n * rr, rl * n * rr)
+    return pl, a, pr, m
+
+
+@pytest.mark.parametrize("dims", [(5, 2, 4, 3, 3), (40, 2, 33, 7, 5), (64, 4, 64, 9, 9)])
+def test_local_apply_and_gmres(dims):
+    """qtt_local_apply equals the explicit local operator (solver.py:136-139)
+    and qtt_local_gmres solves M x = b to rtol (solver.py:186-195)."""
     import torch
 
     from paper_2501_07778_b200 import solver as S
 
-    rng = np.random.default_rng(5)
-    n = 500
-    m = torch.tensor(rng.standard_normal((n, n)) / np.sqrt(n) + 4 * np.eye(n), device="cuda")
-    b = torch.tensor(rng.standard_normal(n), device="cuda")
-    x, ok, its = S._gmres(lambda v: (m @ v.reshape(-1)).reshape(v.shape), b, torch.zeros_like(b), 1e-12)
-    assert ok and its < 100
-    assert float(torch.linalg.vector_norm(m @ x - b) / torch.linalg.vector_norm(b)) <= 1e-11
+    rl, n, rr, ra, rb = dims
+    pl, a, pr, m = _structured_local(rl, n, rr, ra, rb, seed=sum(dims))
+    ap = {"ra": ra, "rb": rb,
+          "aj_ib": torch.tensor(a.transpose(0, 2, 1, 3).reshape(ra * n, n * rb).copy(), device="cuda")}
+    tpl, tpr = torch.tensor(pl, device="cuda"), torch.tensor(pr, device="cuda")
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((rl, n, rr))
+    y = S._local_matvec(tpl, ap, tpr, torch.tensor(x, device="cuda")).cpu().numpy()
+    ref = (m @ x.reshape(-1)).reshape(rl, n, rr)
+    assert np.abs(y - ref).max() <= 1e-13 * np.abs(ref).max()
+    b = rng.standard_normal((rl, n, rr))
+    tb = torch.tensor(b, device="cuda")
+    sol, ok, its = S._gmres(tpl, ap, tpr, tb, torch.zeros_like(tb), 1e-12)
+    assert ok and 0 < its <= 200
+    r = m @ sol.cpu().numpy().reshape(-1) - b.reshape(-1)
+    assert np.linalg.norm(r) <= 1.01e-12 * np.linalg.norm(b)
+    # warm start at the solution: converged before any iteration
+    sol2, ok2, its2 = S._gmres(tpl, ap, tpr, tb, sol, 1e-10)
+    assert ok2 and its2 == 0
+
+
+def test_gmres_early_abort():
+    """A singular-ish operator stalls; abort_early returns unconverged early."""
+    import torch
+
+    from paper_2501_07778_b200 import solver as S
+
+    rl, n, rr, ra, rb = 30, 2, 30, 3, 3
+    pl, a, pr, _ = _structured_local(rl, n, rr, ra, rb, seed=9, shift=0.0)
+    ap = {"ra": ra, "rb": rb,
+          "aj_ib": torch.tensor(a.transpose(0, 2, 1, 3).reshape(ra * n, n * rb).copy(), device="cuda")}
+    tpl, tpr = torch.tensor(pl, device="cuda"), torch.tensor(pr, device="cuda")
+    b = torch.tensor(np.random.default_rng(2).standard_normal((rl, n, rr)), device="cuda")
+    _, ok, its = S._gmres(tpl, ap, tpr, b, torch.zeros_like(b), 1e-14, maxit=400, abort_early=True)
+    assert not ok and its < 400
 
 
 def test_identity_solve_and_zero_rhs():

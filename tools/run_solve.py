@@ -20,6 +20,16 @@ if a.no_solve: sys.exit(0)
 out = S.solve(gsys.K, gsys.f, S.SolverConfig(epsilon=eps, seed=0, local_solver=a.local, max_sweeps=a.max_sweeps, truncation=a.trunc, enrichment_rank=a.rho))
 torch.cuda.synchronize()
 t2 = time.perf_counter()
+calls = (S.PROFILE or {}).pop('calls', [])
+if calls:
+    import collections
+    agg = collections.defaultdict(lambda: [0, 0, 0.0, 0])
+    for kind, rl, ra, rr, its, ok, t in calls:
+        key = (kind, (rl * 2 * rr) // 10000)
+        agg[key][0] += 1; agg[key][1] += its; agg[key][2] += t; agg[key][3] += (not ok)
+    for k in sorted(agg): print('calls', k[0], f'dim~{k[1]*10}k', 'n', agg[k][0], 'its/dim', agg[k][1], 't %.3f' % agg[k][2], 'fail', agg[k][3])
+    fails = [c for c in calls if not c[5]]
+    print('failed gmres:', fails[:30])
 print(json.dumps({'config': a.config, 'd': a.d, 'solve_s': t2 - t1, 'total_s': t2 - t0, 'sweeps': out.sweeps,
                   'residual': out.residual, 'converged': out.converged, 'u_ranks': out.u.ranks,
                   'res_hist': out.residual_history, 'rank_hist': out.rank_history, 'profile': S.PROFILE}), flush=True)
