@@ -905,10 +905,193 @@ cudaStream_t side_stream() {
   return st;
 }
 
+// ------------------------------------------------------------- small QR
+// Whole Householder QR of a small matrix (n <= 64, m <= 256, A in shared
+// memory) in ONE CTA, left-looking and dataflow-ordered: warp w owns columns
+// w, w+16, w+32, w+48 and finishes them in increasing order; a column gets
+// every published reflector applied as soon as its ready flag is up, then
+// its own reflector is formed and published (v in A's lower part, tau,
+// beta on the diagonal).  The serial chain per column is therefore
+// flag -> one column update -> reflector -> flag, with no block barrier;
+// the catch-up of a warp's next column overlaps the other warps' chain.
+// The explicit Q is formed in registers, q_c = H_0 ... H_c e_c, with the
+// owned columns interleaved so their warp reductions overlap.  Replaces the
+// 32-wide cluster panel + compact-WY GEMMs for the small cores of a
+// rounding sweep (~90 us of serial panel latency per 32 columns).
+constexpr int SQ_THREADS = 512, SQ_WARPS = SQ_THREADS / 32, SQ_MAXN = 64, SQ_MAXM = 256;
+constexpr int SQ_CPW = SQ_MAXN / SQ_WARPS;  // columns per warp
+
+// Shared-memory flag handshake with release/acquire semantics at CTA scope
+// (cheaper than a sequentially consistent __threadfence_block()).
+__device__ __forceinline__ void flag_release(volatile int* f) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared((const void*)f);
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(a), "r"(1) : "memory");
+}
+__device__ __forceinline__ int flag_acquire(volatile int* f) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared((const void*)f);
+  int v;
+  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void sq_apply(const double* v, double* col, double tj, int j, int m,
+                                         int lane) {
+  double w = 0.0;
+  for (int r = j + 1 + lane; r < m; r += 32) w = fma(v[r], col[r], w);
+  w = warp_sum(w) + col[j];
+  const double tw = tj * w;
+  for (int r = j + 1 + lane; r < m; r += 32) col[r] = fma(-tw, v[r], col[r]);
+  __syncwarp();
+  if (lane == 0) col[j] -= tw;
+  __syncwarp();
+}
+
+__device__ __forceinline__ void sq_reflect(double* sa, int m, int j, double* tau_s,
+                                           volatile int* ready, int lane) {
+  double* col = sa + (int64_t)j * m;
+  double nrm2 = 0.0;
+  for (int r = j + 1 + lane; r < m; r += 32) nrm2 = fma(col[r], col[r], nrm2);
+  nrm2 = warp_sum(nrm2);
+  const double alpha = col[j];
+  double tau = 0.0, beta = alpha, scal = 1.0;
+  if (nrm2 > 0.0) {
+    const double nrm = sqrt(fma(alpha, alpha, nrm2));
+    beta = alpha >= 0.0 ? -nrm : nrm;
+    tau = (beta - alpha) / beta;
+    scal = 1.0 / (alpha - beta);
+  }
+  for (int r = j + 1 + lane; r < m; r += 32) col[r] *= scal;
+  __syncwarp();
+  if (lane == 0) {
+    col[j] = beta;
+    tau_s[j] = tau;
+  }
+  __syncwarp();
+  if (lane == 0) flag_release(ready + j);
+}
+
+template <int E>
+__global__ void __launch_bounds__(SQ_THREADS) small_qr_kernel(int m, int n, const double* A,
+                                                              int64_t lda, double* Q, int64_t ldq,
+                                                              double* R, int64_t ldr, int dbg) {
+  extern __shared__ double sa[];  // m x n, ld m
+  __shared__ double tau_s[SQ_MAXN];
+  __shared__ int ready_s[SQ_MAXN];
+  __shared__ long long tpub[SQ_MAXN + 4];
+  const long long t0 = clock64();
+  volatile int* ready = ready_s;
+  const int k = min(m, n);
+  for (int idx = threadIdx.x; idx < m * n; idx += SQ_THREADS)
+    sa[idx] = A[(idx % m) + (int64_t)(idx / m) * lda];
+  if (threadIdx.x < SQ_MAXN) ready_s[threadIdx.x] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) tpub[SQ_MAXN] = clock64() - t0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = warp; c < n; c += SQ_WARPS) {
+    double* col = sa + (int64_t)c * m;
+    const int jmax = min(c, k);
+    for (int j = 0; j < jmax; ++j) {
+      while (flag_acquire(ready + j) == 0) {
+      }
+      const double tj = tau_s[j];
+      if (tj != 0.0) sq_apply(sa + (int64_t)j * m, col, tj, j, m, lane);
+    }
+    if (c < k) sq_reflect(sa, m, c, tau_s, ready, lane);
+    if (dbg && lane == 0 && c < SQ_MAXN) tpub[c] = clock64() - t0;
+  }
+  __syncthreads();
+  if (dbg && threadIdx.x == 0) {
+    printf("[sqr] m=%d n=%d load=%lld", m, n, tpub[SQ_MAXN]);
+    for (int c = 0; c < k; c += max(1, k / 8)) printf(" T%d=%lld", c, tpub[c]);
+    printf(" fact_end=%lld\n", clock64() - t0);
+  }
+  if (R) {
+    for (int idx = threadIdx.x; idx < k * n; idx += SQ_THREADS) {
+      const int r = idx % k, c = idx / k;
+      R[r + (int64_t)c * ldr] = (r <= c) ? sa[r + (int64_t)c * m] : 0.0;
+    }
+  }
+  if (!Q) return;
+  // owned Q columns c_i = warp + 16 i (< k), all advanced together
+  double q[SQ_CPW][E];
+  int cmax = -1;
+#pragma unroll
+  for (int i = 0; i < SQ_CPW; ++i) {
+    const int c = warp + SQ_WARPS * i;
+    if (c < k) cmax = c;
+#pragma unroll
+    for (int e = 0; e < E; ++e) q[i][e] = (lane + 32 * e == c) ? 1.0 : 0.0;
+  }
+  for (int j = cmax; j >= 0; --j) {
+    const double tj = tau_s[j];
+    if (tj == 0.0) continue;
+    const double* v = sa + (int64_t)j * m;
+    double vr[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int r = lane + 32 * e;
+      vr[e] = (r < m && r > j) ? v[r] : (r == j ? 1.0 : 0.0);
+    }
+    double w[SQ_CPW];
+#pragma unroll
+    for (int i = 0; i < SQ_CPW; ++i) {
+      w[i] = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) w[i] = fma(vr[e], q[i][e], w[i]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < SQ_CPW; ++i) w[i] += __shfl_xor_sync(0xffffffffu, w[i], o);
+#pragma unroll
+    for (int i = 0; i < SQ_CPW; ++i) {
+      // q_c is still e_c while j > c, and H_j e_c = e_c there
+      if (warp + SQ_WARPS * i < j) continue;
+      const double tw = tj * w[i];
+#pragma unroll
+      for (int e = 0; e < E; ++e) q[i][e] = fma(-tw, vr[e], q[i][e]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < SQ_CPW; ++i) {
+    const int c = warp + SQ_WARPS * i;
+    if (c >= k) continue;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int r = lane + 32 * e;
+      if (r < m) Q[r + (int64_t)c * ldq] = q[i][e];
+    }
+  }
+}
+
+bool small_qr_fits(int m, int n) { return n <= SQ_MAXN && m <= SQ_MAXM; }
+
+int small_qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
+             double* R, int64_t ldr) {
+  const size_t smem = sizeof(double) * (size_t)m * n;
+  static const int dbg = getenv("QTT_SQR_DEBUG") ? 1 : 0;
+  static bool configured = false;
+  if (!configured) {
+    QTT_CUDA(cudaFuncSetAttribute(small_qr_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  SQ_MAXM * SQ_MAXN * 8));
+    QTT_CUDA(cudaFuncSetAttribute(small_qr_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  SQ_MAXM * SQ_MAXN * 8));
+    configured = true;
+  }
+  if (m <= 128)
+    small_qr_kernel<4><<<1, SQ_THREADS, smem, s>>>(m, n, A, lda, Q, ldq, R, ldr, dbg);
+  else
+    small_qr_kernel<8><<<1, SQ_THREADS, smem, s>>>(m, n, A, lda, Q, ldq, R, ldr, dbg);
+  QTT_CHECK_LAUNCH();
+  return kOk;
+}
+
 int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
        double* R, int64_t ldr) {
   if (m <= 0 || n <= 0) return kInvalid;
   const int k = std::min(m, n);
+  static const bool use_small = getenv("QTT_NO_SMALLQR") == nullptr;
+  if (use_small && small_qr_fits(m, n)) return small_qr(s, m, n, A, lda, Q, ldq, R, ldr);
   // Large tall factors: try the GEMM-bound CholeskyQR2 first (certified, falls
   // back to Householder for ill-conditioned / rank-deficient inputs).
   static const bool use_chol = getenv("QTT_NO_CHOLQR") == nullptr;

@@ -48,7 +48,8 @@ def test_gemm_all_transposes():
             assert np.abs(got - want).max() < 1e-12 * np.abs(want).max()
 
 
-@pytest.mark.parametrize("m,n", [(5, 3), (64, 64), (300, 40), (100, 150), (2000, 96), (4100, 70)])
+@pytest.mark.parametrize("m,n", [(5, 3), (64, 64), (300, 40), (100, 150), (2000, 96), (4100, 70),
+                                 (128, 64), (768, 20), (20, 60), (400, 64), (1, 7), (33, 1)])
 def test_qr_explicit(m, n):
     from paper_2501_07778_b200 import _lib
     import ctypes
@@ -271,3 +272,27 @@ def test_qr_cholqr_path_and_fallback(cond):
     assert np.abs(np.tril(r, -1)).max() == 0.0
     assert np.linalg.norm(q @ r - a) <= 1e-13 * np.linalg.norm(a)
     assert np.abs(q.T @ q - np.eye(n)).max() < 1e-12
+
+
+@pytest.mark.parametrize("m,n", [(128, 64), (64, 40), (300, 17)])
+def test_qr_small_rank_deficient(m, n):
+    """Single-CTA QR with zero / repeated columns (tau = 0 reflectors)."""
+    from paper_2501_07778_b200 import _lib
+    import ctypes
+
+    rng = np.random.default_rng(m * n)
+    a = rng.standard_normal((m, n))
+    a[:, 3] = 0.0
+    a[:, 5] = a[:, 1]
+    a[3:, 7 % n] = 0.0
+    k = min(m, n)
+    A = torch.tensor(a.ravel(order="F"), device="cuda")
+    Q = torch.zeros(m * k, dtype=torch.float64, device="cuda")
+    R = torch.zeros(k * n, dtype=torch.float64, device="cuda")
+    _lib.call("qtt_qr", ctypes.c_int64(m), ctypes.c_int64(n), _lib.ptr(A), ctypes.c_int64(m),
+              _lib.ptr(Q), ctypes.c_int64(m), _lib.ptr(R), ctypes.c_int64(k), _lib.stream_handle())
+    q = Q.cpu().numpy().reshape(k, m).T
+    r = R.cpu().numpy().reshape(n, k).T
+    assert np.abs(q @ r - a).max() < 1e-13 * np.abs(a).max() * m
+    assert np.abs(q.T @ q - np.eye(k)).max() < 1e-13 * m
+    assert np.allclose(np.tril(r, -1), 0.0)
