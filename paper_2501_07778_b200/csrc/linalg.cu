@@ -293,6 +293,17 @@ __device__ int jacobi_pair(double* X, int64_t ldx, double* W, int64_t ldw, int p
   return 1;
 }
 
+// Optional rotation floor from the caller's truncation threshold: columns
+// with ||x||^2 < (floor_scale * *floor_dev)^2 / k (the sum over all of them
+// stays below 1e-6 delta^2 for floor_scale = 1e-3 * delta / ||t||) are
+// certain to be discarded by _chop, and rotations among or against them
+// cannot change the kept subspace beyond that energy, so they are skipped.
+__device__ __forceinline__ double jacobi_floor2(const double* floor_dev, double floor_scale, int k) {
+  if (!floor_dev) return 0.0;
+  const double f = floor_scale * *floor_dev;
+  return f * f / (double)max(k, 1);
+}
+
 constexpr int JMAXSWEEPS = 60;
 __device__ int g_jacobi_sweeps;  // sweeps used by the last Jacobi launch (diagnostics)
 constexpr int JTHREADS = 1024;
@@ -300,7 +311,9 @@ constexpr int JTHREADS = 1024;
 // Small problems: one CTA, X and W staged in shared memory.
 __global__ void __launch_bounds__(JTHREADS) jacobi_smem_kernel(int p, int k, double* X,
                                                                 int64_t ldx, double* W,
-                                                                int64_t ldw, double tol) {
+                                                                int64_t ldw, double tol,
+                                                                const double* floor_dev,
+                                                                double floor_scale) {
   extern __shared__ double sm[];
   __shared__ int rotated;
   double* Xs = sm;
@@ -323,7 +336,7 @@ __global__ void __launch_bounds__(JTHREADS) jacobi_smem_kernel(int p, int k, dou
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int w = 0; w < nw; ++w) t += red[w];
-      noise2 = t * kEps * kEps;
+      noise2 = fmax(t * kEps * kEps, jacobi_floor2(floor_dev, floor_scale, k));
     }
     __syncthreads();
   }
@@ -363,7 +376,9 @@ constexpr int JC_THREADS = 512;
 __global__ void __launch_bounds__(JC_THREADS) jacobi_cluster_kernel(int p, int k, double* X,
                                                                      int64_t ldx, double* W,
                                                                      int64_t ldw, double tol,
-                                                                     int px, int pw) {
+                                                                     int px, int pw,
+                                                                     const double* floor_dev,
+                                                                     double floor_scale) {
   extern __shared__ double jc[];
   cg::cluster_group cluster = cg::this_cluster();
   const int cs = (int)cluster.num_blocks();
@@ -406,7 +421,7 @@ __global__ void __launch_bounds__(JC_THREADS) jacobi_cluster_kernel(int p, int k
   cluster.sync();
   double noise2 = 0.0;
   for (int c = 0; c < cs; ++c) noise2 += np2[c];
-  noise2 *= kEps * kEps;
+  noise2 = fmax(noise2 * kEps * kEps, jacobi_floor2(floor_dev, floor_scale, k));
   int round_no = 0;
   for (int sweep = 0; sweep < JMAXSWEEPS; ++sweep) {
     if (tid == 0) any_rot = 0;
@@ -530,7 +545,8 @@ __device__ __forceinline__ void ring_dest(int q, int side, int np, int& dq, int&
 template <int E, int MAXT>
 __global__ void __launch_bounds__(MAXT) jacobi_ring_kernel(int p, int k, double* X, int64_t ldx,
                                                            double* W, int64_t ldw, double tol,
-                                                           int ppc) {
+                                                           int ppc, const double* floor_dev,
+                                                           double floor_scale) {
   extern __shared__ double jr[];  // [2 parity][ppc][2 side][32 E]
   __shared__ double nrm[16];
   __shared__ int anyrot[2];
@@ -579,7 +595,7 @@ __global__ void __launch_bounds__(MAXT) jacobi_ring_kernel(int p, int k, double*
   cluster.sync();
   double noise2 = 0.0;
   for (int c = 0; c < cs; ++c) noise2 += nrm[c];
-  noise2 *= kEps * kEps;
+  noise2 = fmax(noise2 * kEps * kEps, jacobi_floor2(floor_dev, floor_scale, k));
   const double tol2 = tol * tol;
 
   int dq0, ds0, dq1, ds1;
@@ -680,7 +696,7 @@ __global__ void __launch_bounds__(MAXT) jacobi_ring_kernel(int p, int k, double*
 
 template <int E, int MAXT>
 int launch_ring_t(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw,
-                  double tol, int cs, int ppc, size_t smem) {
+                  double tol, int cs, int ppc, size_t smem, const double* fd, double fs) {
   static bool configured = false;
   if (!configured) {
     QTT_CUDA(cudaFuncSetAttribute(jacobi_ring_kernel<E, MAXT>,
@@ -701,14 +717,15 @@ int launch_ring_t(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  QTT_CUDA(cudaLaunchKernelEx(&cfg, jacobi_ring_kernel<E, MAXT>, p, k, X, ldx, W, ldw, tol, ppc));
+  QTT_CUDA(cudaLaunchKernelEx(&cfg, jacobi_ring_kernel<E, MAXT>, p, k, X, ldx, W, ldw, tol, ppc, fd,
+                              fs));
   note_launch();
   return kOk;
 }
 
 // Returns kUnsupported when the problem does not fit the ring kernel.
 int jacobi_ring(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw,
-                double tol) {
+                double tol, const double* fd, double fs) {
   const int L = p + k;
   if (L > JR_MAXL || k < 1) return kUnsupported;
   const int E = (int)ceil_div(L, 32);
@@ -721,11 +738,11 @@ int jacobi_ring(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W,
     if (ppc > maxw || smem > 210 * 1024) continue;
     if (ceil_div(np, ppc) != cs) continue;  // every CTA of the cluster owns >= 1 pair
     switch (Et) {
-      case 4: return launch_ring_t<4, 1024>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem);
-      case 8: return launch_ring_t<8, 1024>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem);
-      case 12: return launch_ring_t<12, 512>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem);
-      case 16: return launch_ring_t<16, 512>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem);
-      default: return launch_ring_t<20, 512>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem);
+      case 4: return launch_ring_t<4, 1024>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem, fd, fs);
+      case 8: return launch_ring_t<8, 1024>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem, fd, fs);
+      case 12: return launch_ring_t<12, 512>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem, fd, fs);
+      case 16: return launch_ring_t<16, 512>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem, fd, fs);
+      default: return launch_ring_t<20, 512>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem, fd, fs);
     }
   }
   return kUnsupported;
@@ -1200,9 +1217,11 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
   return kOk;
 }
 
-static int jacobi_impl(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw);
+static int jacobi_impl(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw,
+                       const double* fd, double fs);
 
-int jacobi(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw) {
+int jacobi(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw,
+           const double* floor_dev, double floor_scale) {
   static const bool dbg = getenv("QTT_JACOBI_DEBUG") != nullptr;
   cudaEvent_t e0, e1;
   if (dbg) {
@@ -1210,7 +1229,7 @@ int jacobi(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int6
     cudaEventCreate(&e1);
     cudaEventRecord(e0, s);
   }
-  const int st = jacobi_impl(s, p, k, X, ldx, W, ldw);
+  const int st = jacobi_impl(s, p, k, X, ldx, W, ldw, floor_dev, floor_scale);
   if (dbg) {
     cudaEventRecord(e1, s);
     cudaEventSynchronize(e1);
@@ -1223,7 +1242,8 @@ int jacobi(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int6
   return st;
 }
 
-static int jacobi_impl(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw) {
+static int jacobi_impl(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw,
+                       const double* fd, double fs) {
   if (p <= 0 || k <= 0) return kInvalid;
   // Off-diagonal cosine threshold.  Rotating below ~32 sqrt(p) eps only churns
   // rounding noise: singular values move at second order (~1e-28) and the
@@ -1233,7 +1253,7 @@ static int jacobi_impl(cudaStream_t s, int p, int k, double* X, int64_t ldx, dou
   static const char* kern = getenv("QTT_JACOBI_KERNEL");
   static const bool legacy = kern && std::string(kern) == "legacy";
   if (!legacy) {
-    const int st = jacobi_ring(s, p, k, X, ldx, W, ldw, tol);
+    const int st = jacobi_ring(s, p, k, X, ldx, W, ldw, tol, fd, fs);
     if (st != kUnsupported) return st;
   }
   const size_t smem = sizeof(double) * ((size_t)p * k + (size_t)k * k);
@@ -1245,7 +1265,7 @@ static int jacobi_impl(cudaStream_t s, int p, int k, double* X, int64_t ldx, dou
       configured = true;
     }
     const int threads = std::min(JTHREADS, std::max(32, ((k + 1) / 2) * 32));
-    jacobi_smem_kernel<<<1, threads, smem, s>>>(p, k, X, ldx, W, ldw, tol);
+    jacobi_smem_kernel<<<1, threads, smem, s>>>(p, k, X, ldx, W, ldw, tol, fd, fs);
     QTT_CHECK_LAUNCH();
     return kOk;
   }
@@ -1274,7 +1294,8 @@ static int jacobi_impl(cudaStream_t s, int p, int k, double* X, int64_t ldx, dou
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    QTT_CUDA(cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel, p, k, X, ldx, W, ldw, tol, px, pw));
+    QTT_CUDA(cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel, p, k, X, ldx, W, ldw, tol, px, pw, fd,
+                                fs));
     note_launch();
     return kOk;
   }

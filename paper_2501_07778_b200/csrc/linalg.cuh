@@ -16,7 +16,11 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
 // One-sided (Hestenes) Jacobi on the p x k column-major matrix X (ldx, in
 // place): X <- X W with W (k x k, ldw) orthogonal, so that the columns of X
 // become mutually orthogonal.  W is initialised to the identity here.
-int jacobi(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw);
+// With floor_dev (device scalar) columns whose squared norm stays below
+// (floor_scale * *floor_dev)^2 / k take no part in rotations (see
+// jacobi_floor2 in linalg.cu); callers pass 1e-3 * delta.
+int jacobi(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw,
+           const double* floor_dev = nullptr, double floor_scale = 0.0);
 
 // Column norms of X (p x k) sorted descending: sigma[k] and perm[k] (device).
 // rank = chop(sigma, delta) (ttcore.py:175-190) with delta read from
