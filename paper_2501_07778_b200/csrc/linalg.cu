@@ -748,6 +748,197 @@ int jacobi_ring(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W,
   return kUnsupported;
 }
 
+// Ring Jacobi for columns too long for shared-memory slots (p + k > 640,
+// k <= 1024): the same warp-per-pair Brent-Luk schedule, but the slots live
+// in a global (L2-resident) workspace, double buffered by round parity, and
+// each round streams its two columns twice (dots over the X rows, then
+// rotate-and-forward), so registers stay O(1).  Loads/stores bypass L1
+// (.cg); the cluster barrier (release/acquire at cluster scope) orders them
+// between CTAs.  Up to 16 CTAs x 32 warps.
+constexpr int GR_U = 8;
+
+__global__ void __launch_bounds__(1024) jacobi_gring_kernel(int p, int k, double* X, int64_t ldx,
+                                                            double* W, int64_t ldw, double tol,
+                                                            int ppc, double* slots,
+                                                            const double* floor_dev,
+                                                            double floor_scale) {
+  __shared__ double nrm[16];
+  __shared__ int anyrot[2];
+  __shared__ double red[32];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cs = (int)cluster.num_blocks();
+  const int cr = (int)cluster.block_rank();
+  const int kp = k + (k & 1), np = kp / 2;
+  const int64_t L = (int64_t)p + k;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = cr * ppc + warp;
+  const bool active = q < np;
+  const int c0 = q, c1 = kp - 1 - q;
+  auto slot = [&](int par, int qq, int side) {
+    return slots + (((int64_t)par * np + qq) * 2 + side) * L;
+  };
+  double acc = 0.0;
+  if (active) {
+    double* s0 = slot(0, q, 0);
+    double* s1 = slot(0, q, 1);
+    for (int64_t t = lane; t < L; t += 32) {
+      double a = 0.0, b = 0.0;
+      if (t < p) {
+        a = X[t + (int64_t)c0 * ldx];
+        b = c1 < k ? X[t + (int64_t)c1 * ldx] : 0.0;
+        acc = fma(a, a, fma(b, b, acc));
+      } else {
+        a = (t - p == c0) ? 1.0 : 0.0;
+        b = (t - p == c1 && c1 < k) ? 1.0 : 0.0;
+      }
+      __stcg(s0 + t, a);
+      __stcg(s1 + t, b);
+    }
+  }
+  if (threadIdx.x < 2) anyrot[threadIdx.x] = 0;
+  acc = warp_sum(acc);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if ((int)threadIdx.x < cs) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    cluster.map_shared_rank(nrm, (int)threadIdx.x)[cr] = t;
+  }
+  cluster.sync();
+  double noise2 = 0.0;
+  for (int c = 0; c < cs; ++c) noise2 += nrm[c];
+  noise2 = fmax(noise2 * kEps * kEps, jacobi_floor2(floor_dev, floor_scale, k));
+  const double tol2 = tol * tol;
+  int dq0, ds0, dq1, ds1;
+  ring_dest(q, 0, np, dq0, ds0);
+  ring_dest(q, 1, np, dq1, ds1);
+  int sweep = 0, rn = 0;
+  for (; sweep < JMAXSWEEPS; ++sweep) {
+    int rotated = 0;
+    for (int r = 0; r < kp - 1; ++r, ++rn) {
+      if (active) {
+        const double* u = slot(rn & 1, q, 0);
+        const double* v = slot(rn & 1, q, 1);
+        double* du = slot((rn + 1) & 1, dq0, ds0);
+        double* dv = slot((rn + 1) & 1, dq1, ds1);
+        // 8 independent loads per lane in flight (L2 latency bound otherwise)
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int t0 = lane; t0 < p; t0 += 32 * GR_U) {
+          double xs[GR_U], ys[GR_U];
+#pragma unroll
+          for (int e = 0; e < GR_U; ++e) {
+            const int t = t0 + 32 * e;
+            xs[e] = t < p ? __ldcg(u + t) : 0.0;
+            ys[e] = t < p ? __ldcg(v + t) : 0.0;
+          }
+#pragma unroll
+          for (int e = 0; e < GR_U; ++e) {
+            a = fma(xs[e], xs[e], a);
+            b = fma(ys[e], ys[e], b);
+            g = fma(xs[e], ys[e], g);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          g += __shfl_xor_sync(0xffffffffu, g, o);
+        }
+        double c = 1.0, sn = 0.0;
+        if (g != 0.0 && a >= noise2 && b >= noise2 && g * g > tol2 * a * b) {
+          const double zeta = (b - a) * rcp_nr(2.0 * g);
+          const double az = fabs(zeta);
+          double t;
+          if (az < 1e100) {
+            const double w = fma(zeta, zeta, 1.0);
+            t = rcp_nr(az + w * rsqrt_nr(w));
+          } else {
+            t = 0.5 * rcp_nr(az);
+          }
+          t = zeta >= 0.0 ? t : -t;
+          c = rsqrt_nr(fma(t, t, 1.0));
+          sn = c * t;
+          rotated = 1;
+        }
+        for (int64_t t0 = lane; t0 < L; t0 += 32 * GR_U) {
+          double xs[GR_U], ys[GR_U];
+#pragma unroll
+          for (int e = 0; e < GR_U; ++e) {
+            const int64_t t = t0 + 32 * e;
+            xs[e] = t < L ? __ldcg(u + t) : 0.0;
+            ys[e] = t < L ? __ldcg(v + t) : 0.0;
+          }
+#pragma unroll
+          for (int e = 0; e < GR_U; ++e) {
+            const int64_t t = t0 + 32 * e;
+            if (t < L) {
+              __stcg(du + t, c * xs[e] - sn * ys[e]);
+              __stcg(dv + t, sn * xs[e] + c * ys[e]);
+            }
+          }
+        }
+        if (r == kp - 2 && rotated && lane < cs)
+          (lane == cr ? anyrot : cluster.map_shared_rank(anyrot, lane))[sweep & 1] = 1;
+      }
+      cluster.sync();
+    }
+    const int more = anyrot[sweep & 1];
+    __syncthreads();
+    if (threadIdx.x == 0) anyrot[sweep & 1] = 0;
+    if (!more) break;
+  }
+  if (cr == 0 && threadIdx.x == 0) g_jacobi_sweeps = min(sweep + 1, JMAXSWEEPS);
+  if (active) {
+    const double* u = slot(rn & 1, q, 0);
+    const double* v = slot(rn & 1, q, 1);
+    for (int64_t t = lane; t < L; t += 32) {
+      const double x = __ldcg(u + t), y = __ldcg(v + t);
+      if (t < p) {
+        X[t + (int64_t)c0 * ldx] = x;
+        if (c1 < k) X[t + (int64_t)c1 * ldx] = y;
+      } else {
+        W[(t - p) + (int64_t)c0 * ldw] = x;
+        if (c1 < k) W[(t - p) + (int64_t)c1 * ldw] = y;
+      }
+    }
+  }
+  cluster.sync();
+}
+
+int jacobi_gring(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw,
+                 double tol, const double* fd, double fs) {
+  const int np = (k + (k & 1)) / 2;
+  if (k < 2 || np > 16 * 32) return kUnsupported;
+  int cs = (int)ceil_div(np, 32);
+  const int ppc = (int)ceil_div(np, cs);
+  cs = (int)ceil_div(np, ppc);
+  static bool configured = false;
+  if (!configured) {
+    QTT_CUDA(cudaFuncSetAttribute(jacobi_gring_kernel,
+                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+  }
+  double* slots;
+  QTT_CUDA(cudaMallocAsync(&slots, sizeof(double) * 4 * (size_t)np * ((size_t)p + k), s));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs, 1, 1);
+  cfg.blockDim = dim3(ppc * 32, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  QTT_CUDA(cudaLaunchKernelEx(&cfg, jacobi_gring_kernel, p, k, X, ldx, W, ldw, tol, ppc, slots, fd,
+                              fs));
+  note_launch();
+  QTT_CUDA(cudaFreeAsync(slots, s));
+  return kOk;
+}
+
 // Large problems: cooperative grid, columns stay in global memory (L2).
 __global__ void __launch_bounds__(256) jacobi_grid_kernel(int p, int k, double* X, int64_t ldx,
                                                           double* W, int64_t ldw, double tol,
@@ -1253,7 +1444,8 @@ static int jacobi_impl(cudaStream_t s, int p, int k, double* X, int64_t ldx, dou
   static const char* kern = getenv("QTT_JACOBI_KERNEL");
   static const bool legacy = kern && std::string(kern) == "legacy";
   if (!legacy) {
-    const int st = jacobi_ring(s, p, k, X, ldx, W, ldw, tol, fd, fs);
+    int st = jacobi_ring(s, p, k, X, ldx, W, ldw, tol, fd, fs);
+    if (st == kUnsupported) st = jacobi_gring(s, p, k, X, ldx, W, ldw, tol, fd, fs);
     if (st != kUnsupported) return st;
   }
   const size_t smem = sizeof(double) * ((size_t)p * k + (size_t)k * k);

@@ -7,7 +7,7 @@ sys.path.insert(0, '.')
 import numpy as np, torch
 from paper_2501_07778_b200 import _lib
 
-for k in (24, 60, 100, 150, 200, 224, 300):
+for k in [int(a) for a in sys.argv[1:]] or (24, 60, 100, 150, 200, 224, 300, 400, 468, 600):
     rng = np.random.default_rng(k)
     u0, _ = np.linalg.qr(rng.standard_normal((k, k)))
     v0, _ = np.linalg.qr(rng.standard_normal((k, k)))
