@@ -108,10 +108,6 @@ void reduce_left(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vect
 
 }  // namespace
 
-// Jacobi rotation floor relative to the truncation threshold delta
-// (linalg.cuh: columns below 1e-3 delta / sqrt(k) are certainly discarded).
-constexpr double kFloorFrac = 1e-3;
-
 // Rounding core on merged order-3 slots (shared by qtt_round and the solver).
 int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vector<int64_t>& n,
                 const std::vector<int64_t>& off, double* work, double eps) {
@@ -160,7 +156,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
         QTT_TRY(dgemm(s, 0, 1, mc, N, N, 1.0, next, mc, tr.p, N, 0.0, tc.p, mc, kGemmLowB));
       } else {
         QTT_TRY(transpose(s, N, N, tr.p, N, xb.p, N));  // X = R^T
-        QTT_TRY(jacobi(s, N, N, xb.p, N, wb.p, N, norm_dev, kFloorFrac * dscale));
+        QTT_TRY(jacobi(s, N, N, xb.p, N, wb.p, N));
         QTT_TRY(sort_chop(s, N, N, xb.p, N, sigma, perm, norm_dev, dscale, N, 1, flags + 1));
         QTT_TRY(fetch(s, flags + 1, &newk));
         QTT_TRY(gather_columns(s, N, newk, wb.p, N, perm, wp.p, N));
@@ -181,7 +177,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
         QTT_TRY(set_identity(s, m, m, core, m));
       } else {
         QTT_TRY(copy_matrix(s, m, m, tr.p, m, xb.p, m));  // X = R2 (S = R2^T)
-        QTT_TRY(jacobi(s, m, m, xb.p, m, wb.p, m, norm_dev, kFloorFrac * dscale));
+        QTT_TRY(jacobi(s, m, m, xb.p, m, wb.p, m));
         QTT_TRY(sort_chop(s, m, m, xb.p, m, sigma, perm, norm_dev, dscale, m, 1, flags + 1));
         QTT_TRY(fetch(s, flags + 1, &newk));
         QTT_TRY(gather_columns(s, m, newk, wb.p, m, perm, wp.p, m));
