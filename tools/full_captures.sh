@@ -1,12 +1,4 @@
-# Round-end measurement artefacts (run on the GPU box from the repo root):
-# bench line, ncu launch list of the config-2 step, full captures of the
-# top DMMA GEMM launch and of the matvec kernel.
-set -x
 mkdir -p gpurun_out
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/step_launches.csv \
-    python bench.py --steps 1 --warmup 1 --no-extras --no-cpu-baseline > gpurun_out/ncu_step.log 2>&1
-python tools/agg_launches.py gpurun_out/step_launches.csv > gpurun_out/step_launches.txt 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 100 -c 1 \
     -o gpurun_out/gemm_full python tools/one_pair.py 16x128 1 > gpurun_out/ncu_gemm.log 2>&1
 timeout 300 ncu --set full --clock-control none -k regex:core_product_kernel -c 1 \
