@@ -187,7 +187,7 @@ int chol_near_identity(cudaStream_t s, int n, double* G, int64_t ldg, double* U,
 // panel k+1.  Dependencies: a_k after b_{k-1} (both update block row k+1),
 // b_k after panel k; disjoint writes otherwise.
 int chol_upper(cudaStream_t s, int n, double* G, int64_t ldg, double* rblk, int* bad) {
-  static cudaEvent_t ev[6] = {};
+  thread_local cudaEvent_t ev[6] = {};
   if (!ev[0])
     for (auto& e : ev) QTT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   cudaEvent_t *evP = ev, *evB = ev + 2, evStart = ev[4], evEnd = ev[5];

@@ -1102,7 +1102,7 @@ int set_identity(cudaStream_t s, int rows, int cols, double* A, int64_t lda) {
 
 // Side stream for the look-ahead panel factorisation (one per process).
 cudaStream_t side_stream() {
-  static cudaStream_t st = nullptr;
+  thread_local cudaStream_t st = nullptr;
   if (!st) {
     // highest priority: the panel (critical path) is scheduled ahead of the
     // trailing-update GEMM blocks as soon as SMs free up
@@ -1331,7 +1331,7 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
   // Look-ahead: after panel p, update only panel p+1's columns, factor panel
   // p+1 on a side stream while the rest of the trailing matrix is updated,
   // so the latency-bound panel overlaps the DMMA update.
-  static cudaEvent_t ev_cols = nullptr, ev_panel = nullptr;
+  thread_local cudaEvent_t ev_cols = nullptr, ev_panel = nullptr;
   if (!ev_cols) {
     QTT_CUDA(cudaEventCreateWithFlags(&ev_cols, cudaEventDisableTiming));
     QTT_CUDA(cudaEventCreateWithFlags(&ev_panel, cudaEventDisableTiming));

@@ -104,7 +104,7 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
   // solves of block k only the next block column is updated, the next
   // diagonal block is factorised on the side stream while the rest of the
   // Schur complement is updated here.
-  static cudaEvent_t ev_col = nullptr, ev_diag = nullptr;
+  thread_local cudaEvent_t ev_col = nullptr, ev_diag = nullptr;
   if (!ev_col) {
     QTT_CUDA(cudaEventCreateWithFlags(&ev_col, cudaEventDisableTiming));
     QTT_CUDA(cudaEventCreateWithFlags(&ev_diag, cudaEventDisableTiming));
