@@ -7,6 +7,7 @@ point raises when the shared library or a CUDA device is missing.
 
 from __future__ import annotations
 
+import concurrent.futures
 import ctypes
 import os
 
@@ -161,3 +162,39 @@ def gemm_profile_stop() -> tuple:
     call("qtt_profile_gemm_read", ctypes.byref(f), ctypes.byref(ms), ctypes.byref(n))
     call("qtt_profile_gemm", ctypes.c_int32(0))
     return f.value, ms.value, n.value
+
+
+_POOL = None
+_STREAMS: list = []
+
+
+def run_concurrent(jobs):
+    """Run independent TT chains (fn(arg) -> TT object) concurrently, one CUDA stream
+    and one host thread each (the C-ABI calls release the GIL; each chain's
+    host synchronisations then overlap the others' kernels).  Inputs were
+    produced on the caller's stream, which every chain stream waits for; the
+    caller's stream waits for all chains before the results are used."""
+    global _POOL, _STREAMS
+    dev = torch.cuda.current_device()
+    if _POOL is None:
+        _POOL = concurrent.futures.ThreadPoolExecutor(max_workers=6, thread_name_prefix="qtt-chain")
+    if len(_STREAMS) < len(jobs) or _STREAMS[0].device.index != dev:
+        _STREAMS = [torch.cuda.Stream(device=dev) for _ in range(max(6, len(jobs)))]
+    main = torch.cuda.current_stream()
+
+    def run(fn, arg, stream):
+        torch.cuda.set_device(dev)
+        stream.wait_stream(main)
+        with torch.cuda.stream(stream):
+            out = fn(arg)
+        for item in (out if isinstance(out, tuple) else (out,)):
+            t = getattr(item, "data", item)
+            if isinstance(t, torch.Tensor) and t.is_cuda:
+                t.record_stream(main)
+        return out
+
+    futs = [_POOL.submit(run, fn, arg, _STREAMS[i]) for i, (fn, arg) in enumerate(jobs)]
+    outs = [f.result() for f in futs]
+    for i in range(len(jobs)):
+        main.wait_stream(_STREAMS[i])
+    return outs

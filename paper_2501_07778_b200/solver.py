@@ -138,6 +138,38 @@ def residual(K: TTMatrix, u: TTVector, f: TTVector, rounding_eps=None) -> float:
     return tt_norm(y) / fn
 
 
+_SIDE = {}
+
+
+class _AsyncResidual:
+    """residual(K, u, f) on the dense path, enqueued on a side stream
+    (same operations and order, so the same value); value() waits."""
+
+    def __init__(self, K: TTMatrix, u: TTVector, fd: torch.Tensor):
+        dev = torch.cuda.current_device()
+        side = _SIDE.get(dev)
+        if side is None:
+            side = _SIDE[dev] = torch.cuda.Stream(device=dev)
+        main = torch.cuda.current_stream()
+        side.wait_stream(main)
+        u.data.record_stream(side)
+        fd.record_stream(side)
+        K.data.record_stream(side)
+        with torch.cuda.stream(side):
+            ud = tt_contract_device(u)
+            r = apply_tt_matrix(K, ud) - fd
+            self._val = torch.linalg.vector_norm(r) / torch.linalg.vector_norm(fd)
+            self._ev = torch.cuda.Event()
+            self._ev.record(side)
+
+    def ready(self) -> bool:
+        return self._ev.query()
+
+    def value(self) -> float:
+        self._ev.synchronize()
+        return float(self._val)
+
+
 # ------------------------------------------------- interface contractions
 
 
@@ -478,10 +510,40 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig, x0: TTVector | None = Non
     residual_rule = cfg.truncation == "residual"
     tol_loc = cfg.trunc_factor * cfg.epsilon / np.sqrt(d)
     sweeps_done = 0
+    # With the residual truncation rule nothing in sweep s+1 depends on the
+    # residual of sweep s except the decision to stop, so that residual is
+    # evaluated on a side stream while sweep s+1 starts; the sweep is
+    # abandoned at the next core boundary once the residual shows convergence
+    # (the returned u is then the converged iterate of sweep s, exactly as in
+    # the sequential order).
+    speculate = residual_rule and d <= _DENSE_RESIDUAL_BITS
+    pending = None  # (async residual, u, sweep index)
+    fd_cache = []
+    u_final = None
+
+    def poll(block=False):
+        nonlocal pending, res, sweeps_done, u_final
+        if pending is None or not (block or pending[0].ready()):
+            return False
+        ares, pu, ps = pending
+        pending = None
+        res = ares.value()
+        residual_history.append(float(res))
+        if _TRACE:
+            print(f"[amen] sweep {ps + 1} res {res:.3e} max rank {rank_history[ps]} "
+                  f"t {time.perf_counter() - t0:.2f}s", flush=True)
+        if res <= cfg.epsilon:
+            sweeps_done = ps + 1
+            u_final = pu
+            return True
+        return False
+
     for sweep in range(cfg.max_sweeps):
         rtol_local = max(0.02 * cfg.epsilon * adapt, 1e-13)  # solver.py:296
         # ---------------- forward: solve + enrich ----------------
         for k in range(d):
+            if poll():
+                break
             rhs = _local_rhs(psi_l[k], F[k], psi_r[k + 1])
             xk = _solve_local(phi_l[k], A[k], phi_r[k + 1], rhs, x_cur=x[k], cfg=cfg, rtol=rtol_local)
             x[k] = xk
@@ -504,10 +566,14 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig, x0: TTVector | None = Non
                     psi_l[k + 1] = _psi_left(psi_l[k], x[k], F[k])
                     za_l[k + 1] = _phi_left(za_l[k], z[k], A[k], x[k])
                     zf_l[k + 1] = _psi_left(zf_l[k], z[k], F[k])
+        if u_final is not None:
+            break
         # ---------------- backward: solve + truncate ----------------
         xnorm = float(torch.linalg.vector_norm(x[d - 1]))
         delta = cfg.trunc_factor * cfg.epsilon * adapt * max(xnorm, 1e-300) / np.sqrt(d)
         for k in range(d - 1, -1, -1):
+            if poll():
+                break
             rhs = _local_rhs(psi_l[k], F[k], psi_r[k + 1])
             xk, mcm = _solve_local(phi_l[k], A[k], phi_r[k + 1], rhs, keep=True, x_cur=x[k], cfg=cfg,
                                    rtol=rtol_local)
@@ -531,9 +597,16 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig, x0: TTVector | None = Non
                     zf_r[k] = _psi_right(zf_r[k + 1], z[k], F[k])
             else:
                 x[k] = xk
+        if u_final is not None or poll(block=True):
+            break
         sweeps_done = sweep + 1
         rank_history.append(max(c.shape[0] for c in x[1:]) if d > 1 else 1)
         u = _concat(TTVector, x)
+        if speculate and sweep + 1 < cfg.max_sweeps:
+            if not fd_cache:
+                fd_cache.append(tt_contract_device(f))
+            pending = (_AsyncResidual(K, u, fd_cache[0]), u, sweep)
+            continue
         with _phase("residual"):
             res = residual(K, u, f)
         residual_history.append(float(res))
@@ -546,7 +619,8 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig, x0: TTVector | None = Non
             adapt *= 0.25
         res_prev = res
 
-    u = _concat(TTVector, x)
+    poll(block=True)
+    u = u_final if u_final is not None else _concat(TTVector, x)
     if res <= cfg.epsilon:
         u, res = _final_compress(K, f, u, res, cfg.epsilon)
     return SolveOutcome(u, float(res), sweeps_done, tuple(rank_history), tuple(residual_history),
@@ -557,9 +631,15 @@ def _final_compress(K, f, u, res, epsilon):
     """Loosest re-rounding that keeps the residual within epsilon (solver.py:392-409)."""
     if max(epsilon - res, 0.0) <= 0.0:
         return u, res
-    for factor in (0.5, 0.25, 0.1, 0.03, 0.01, 0.003):
+    # the six candidates are independent: evaluate them concurrently (own
+    # stream and host thread each) and keep the first passing one in the
+    # reference's order
+    def candidate(factor):
         cand = tt_round(u, factor * epsilon)
-        r = residual(K, cand, f)
+        return cand, residual(K, cand, f)
+
+    outs = _lib.run_concurrent([(candidate, fac) for fac in (0.5, 0.25, 0.1, 0.03, 0.01, 0.003)])
+    for cand, r in outs:
         if r <= epsilon:
             return cand, r
     return u, res
