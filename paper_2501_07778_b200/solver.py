@@ -82,6 +82,12 @@ class SolverConfig:
     # whose truncated local solution still satisfies the local system to
     # trunc_factor * epsilon / sqrt(d) (no stall adaptation needed).
     truncation: str = "reference"
+    # Extension (0 = reference rule): with the residual truncation rule, the
+    # local tolerance is relaxed to local_rtol_factor * (latest known global
+    # residual) while that exceeds the reference's 0.02 * epsilon, i.e.
+    # inexact local solves in the early sweeps (no accuracy is lost at
+    # convergence: the bound tightens with the residual).
+    local_rtol_factor: float = 0.0
 
     def __post_init__(self):
         if self.epsilon <= 0:
@@ -540,6 +546,8 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig, x0: TTVector | None = Non
 
     for sweep in range(cfg.max_sweeps):
         rtol_local = max(0.02 * cfg.epsilon * adapt, 1e-13)  # solver.py:296
+        if residual_rule and cfg.local_rtol_factor > 0.0 and residual_history:
+            rtol_local = max(rtol_local, min(cfg.local_rtol_factor * residual_history[-1], 1e-4))
         # ---------------- forward: solve + enrich ----------------
         for k in range(d):
             if poll():
