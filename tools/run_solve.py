@@ -5,9 +5,10 @@ from paper_2501_07778_b200.configs import build_system
 from paper_2501_07778_b200 import solver as S
 ap = argparse.ArgumentParser(); ap.add_argument('--config', type=int, default=1); ap.add_argument('--d', type=int, default=None)
 ap.add_argument('--max-sweeps', type=int, default=40); ap.add_argument('--no-solve', action='store_true'); ap.add_argument('--dense-bits', type=int, default=22)
-ap.add_argument('--trunc', default='reference'); ap.add_argument('--rho', type=int, default=4); ap.add_argument('--local', default='direct'); ap.add_argument('--rtol-factor', type=float, default=0.0)
+ap.add_argument('--trunc', default='reference'); ap.add_argument('--rho', type=int, default=4); ap.add_argument('--local', default='direct'); ap.add_argument('--rtol-factor', type=float, default=0.0); ap.add_argument('--iter-min', type=int, default=None)
 a = ap.parse_args()
 S._DENSE_RESIDUAL_BITS = a.dense_bits
+if a.iter_min is not None: S._ITERATIVE_MIN_DIM = a.iter_min
 import os
 if os.environ.get('QTT_SOLVER_PROFILE'): S.PROFILE = {}
 tm = {}
