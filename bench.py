@@ -176,6 +176,19 @@ def _dist_env():
     return world, rank, local
 
 
+def job_throughput(local_ms: float, steps: int, flops_per_replica: float, dist, world: int, dev):
+    """Whole-job throughput of N independent replicas: the step time is the
+    MAX over ranks of the device-timed total (all_reduce MAX), the work is
+    world x one replica's nominal flops.  Returns (ms_per_step, GFLOP/s)."""
+    import torch
+
+    t = torch.tensor([local_ms], dtype=torch.float64, device=dev)
+    if dist is not None and world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / steps
+    return ms_per_step, world * flops_per_replica / (ms_per_step * 1e-3) / 1e9
+
+
 def run_ours(args):
     import torch
 
@@ -235,12 +248,7 @@ def run_ours(args):
         total_ms += e0.elapsed_time(e1)
     launches = _lib.launch_count() - launches0
     clk = clocks.stop()
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
-    ms_per_step = max_ms / args.steps
-    value = world * flops / (ms_per_step * 1e-3) / 1e9
+    ms_per_step, value = job_throughput(total_ms, args.steps, flops, dist, world, dev)
 
     # ---- end to end through the public API with host buffers
     e2e_ms = 0.0

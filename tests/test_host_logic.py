@@ -97,3 +97,36 @@ def test_configs_specs():
     assert mat.modulus_field(np.array(0.25), np.array(0.25)) == pytest.approx(1.5)
     meshes, mat, body, eps = config(5)
     assert len(meshes) == 3 and meshes[2].tag("top") == "clamped" and mat.mode == "plane-strain"
+
+
+def _throughput_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    import bench
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        local_ms = 10.0 * (rank + 1)  # rank 1 is the slow replica
+        out[rank] = bench.job_throughput(local_ms, 2, 1e9, dist, world, torch.device("cpu"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_replica_throughput_max_over_ranks_gloo():
+    """bench.py's N>1 path (replicas, max-over-ranks step time) with the gloo
+    backend and world_size 2 on CPU."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_throughput_worker, args=(2, port, out), nprocs=2, join=True)
+    for rank in range(2):
+        ms, value = out[rank]
+        assert ms == pytest.approx(10.0)  # max(10, 20) ms over 2 steps
+        assert value == pytest.approx(2 * 1e9 / 10e-3 / 1e9)
