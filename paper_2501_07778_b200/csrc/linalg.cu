@@ -905,6 +905,214 @@ __global__ void __launch_bounds__(1024) jacobi_gring_kernel(int p, int k, double
   cluster.sync();
 }
 
+// Ring Jacobi for long columns (p + k in (640, 1024]) with SINGLE-buffered
+// shared-memory slots: every pair rotates its two columns in place, then the
+// ring migration is done as a PULL in two halves (each lane stages half a
+// column pair in registers, cluster barrier, writes its own slot), so a
+// cluster of <= 16 CTAs holds the whole augmented matrix in shared memory
+// (~15 KB per pair) at three cluster barriers per round and no L2 traffic.
+template <int EH>
+__global__ void __launch_bounds__(512) jacobi_pring_kernel(int p, int k, double* X, int64_t ldx,
+                                                           double* W, int64_t ldw, double tol,
+                                                           int ppc, const double* floor_dev,
+                                                           double floor_scale) {
+  extern __shared__ double jp[];  // [ppc][2][L]
+  __shared__ double nrm[16];
+  __shared__ int anyrot[2];
+  __shared__ double red[32];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cs = (int)cluster.num_blocks();
+  const int cr = (int)cluster.block_rank();
+  const int kp = k + (k & 1), np = kp / 2;
+  const int L = p + k;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = cr * ppc + warp;
+  const bool active = q < np;
+  const int c0 = q, c1 = kp - 1 - q;
+  double* const u = jp + (size_t)warp * 2 * L;
+  double* const v = u + L;
+  double acc = 0.0;
+  if (active) {
+    for (int t = lane; t < L; t += 32) {
+      double a = 0.0, b = 0.0;
+      if (t < p) {
+        a = X[t + (int64_t)c0 * ldx];
+        b = c1 < k ? X[t + (int64_t)c1 * ldx] : 0.0;
+        acc = fma(a, a, fma(b, b, acc));
+      } else {
+        a = (t - p == c0) ? 1.0 : 0.0;
+        b = (t - p == c1 && c1 < k) ? 1.0 : 0.0;
+      }
+      u[t] = a;
+      v[t] = b;
+    }
+  }
+  if (threadIdx.x < 2) anyrot[threadIdx.x] = 0;
+  acc = warp_sum(acc);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if ((int)threadIdx.x < cs) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    cluster.map_shared_rank(nrm, (int)threadIdx.x)[cr] = t;
+  }
+  cluster.sync();
+  double noise2 = 0.0;
+  for (int c = 0; c < cs; ++c) noise2 += nrm[c];
+  noise2 = fmax(noise2 * kEps * kEps, jacobi_floor2(floor_dev, floor_scale, k));
+  const double tol2 = tol * tol;
+  // pull sources (inverse of ring_dest)
+  int sq0, ss0, sq1, ss1;
+  if (np == 1) {
+    sq0 = 0; ss0 = 0; sq1 = 0; ss1 = 1;
+  } else {
+    sq0 = q == 0 ? 0 : (q == np - 1 ? np - 1 : q + 1);
+    ss0 = (q == np - 1 && q != 0) ? 1 : 0;
+    sq1 = q == 0 ? 1 : q - 1;
+    ss1 = q == 0 ? 0 : 1;
+  }
+  const double* src0 = nullptr;
+  const double* src1 = nullptr;
+  if (active) {
+    const double* b0 = sq0 / ppc == cr ? jp : cluster.map_shared_rank(jp, sq0 / ppc);
+    const double* b1 = sq1 / ppc == cr ? jp : cluster.map_shared_rank(jp, sq1 / ppc);
+    src0 = b0 + ((size_t)(sq0 % ppc) * 2 + ss0) * L;
+    src1 = b1 + ((size_t)(sq1 % ppc) * 2 + ss1) * L;
+  }
+  const int half = (L + 1) / 2;
+  int sweep = 0;
+  for (; sweep < JMAXSWEEPS; ++sweep) {
+    int rotated = 0;
+    for (int r = 0; r < kp - 1; ++r) {
+      if (active) {
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int t = lane; t < p; t += 32) {
+          const double x = u[t], y = v[t];
+          a = fma(x, x, a);
+          b = fma(y, y, b);
+          g = fma(x, y, g);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          g += __shfl_xor_sync(0xffffffffu, g, o);
+        }
+        if (g != 0.0 && a >= noise2 && b >= noise2 && g * g > tol2 * a * b) {
+          const double zeta = (b - a) * rcp_nr(2.0 * g);
+          const double az = fabs(zeta);
+          double t;
+          if (az < 1e100) {
+            const double w = fma(zeta, zeta, 1.0);
+            t = rcp_nr(az + w * rsqrt_nr(w));
+          } else {
+            t = 0.5 * rcp_nr(az);
+          }
+          t = zeta >= 0.0 ? t : -t;
+          const double c = rsqrt_nr(fma(t, t, 1.0));
+          const double sn = c * t;
+          for (int t2 = lane; t2 < L; t2 += 32) {
+            const double x = u[t2], y = v[t2];
+            u[t2] = c * x - sn * y;
+            v[t2] = sn * x + c * y;
+          }
+          rotated = 1;
+        }
+        if (r == kp - 2 && rotated && lane < cs)
+          (lane == cr ? anyrot : cluster.map_shared_rank(anyrot, lane))[sweep & 1] = 1;
+      }
+      cluster.sync();  // B1: all rotations (and flags) done
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int lo = hh * half, hi = min(L, lo + half);
+        double ru[EH], rv[EH];
+        if (active) {
+#pragma unroll
+          for (int e = 0; e < EH; ++e) {
+            const int t = lo + lane + 32 * e;
+            ru[e] = t < hi ? src0[t] : 0.0;
+            rv[e] = t < hi ? src1[t] : 0.0;
+          }
+        }
+        cluster.sync();  // B2/B3: every reader of this half is done
+        if (active) {
+#pragma unroll
+          for (int e = 0; e < EH; ++e) {
+            const int t = lo + lane + 32 * e;
+            if (t < hi) {
+              u[t] = ru[e];
+              v[t] = rv[e];
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    const int more = anyrot[sweep & 1];
+    __syncthreads();
+    if (threadIdx.x == 0) anyrot[sweep & 1] = 0;
+    if (!more) break;
+  }
+  if (cr == 0 && threadIdx.x == 0) g_jacobi_sweeps = min(sweep + 1, JMAXSWEEPS);
+  if (active) {
+    for (int t = lane; t < L; t += 32) {
+      if (t < p) {
+        X[t + (int64_t)c0 * ldx] = u[t];
+        if (c1 < k) X[t + (int64_t)c1 * ldx] = v[t];
+      } else {
+        W[(t - p) + (int64_t)c0 * ldw] = u[t];
+        if (c1 < k) W[(t - p) + (int64_t)c1 * ldw] = v[t];
+      }
+    }
+  }
+  cluster.sync();
+}
+
+template <int EH>
+int launch_pring_t(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw,
+                   double tol, int cs, int ppc, size_t smem, const double* fd, double fs) {
+  static bool configured = false;
+  if (!configured) {
+    QTT_CUDA(cudaFuncSetAttribute(jacobi_pring_kernel<EH>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
+    QTT_CUDA(cudaFuncSetAttribute(jacobi_pring_kernel<EH>,
+                                  cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs, 1, 1);
+  cfg.blockDim = dim3(ppc * 32, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cs;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  QTT_CUDA(cudaLaunchKernelEx(&cfg, jacobi_pring_kernel<EH>, p, k, X, ldx, W, ldw, tol, ppc, fd, fs));
+  note_launch();
+  return kOk;
+}
+
+int jacobi_pring(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw,
+                 double tol, const double* fd, double fs) {
+  const int L = p + k;
+  if (L > 1024 || k < 2) return kUnsupported;
+  const int EH = (int)ceil_div((L + 1) / 2, 32);
+  const int np = (k + (k & 1)) / 2;
+  for (int cs = 1; cs <= 16; ++cs) {
+    const int ppc = (int)ceil_div(np, cs);
+    const size_t smem = sizeof(double) * 2 * (size_t)ppc * L;
+    if (ppc > 16 || smem > 226 * 1024) continue;
+    if (ceil_div(np, ppc) != cs) continue;
+    if (EH <= 12) return launch_pring_t<12>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem, fd, fs);
+    return launch_pring_t<16>(s, p, k, X, ldx, W, ldw, tol, cs, ppc, smem, fd, fs);
+  }
+  return kUnsupported;
+}
+
 int jacobi_gring(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw,
                  double tol, const double* fd, double fs) {
   const int np = (k + (k & 1)) / 2;
@@ -1445,6 +1653,7 @@ static int jacobi_impl(cudaStream_t s, int p, int k, double* X, int64_t ldx, dou
   static const bool legacy = kern && std::string(kern) == "legacy";
   if (!legacy) {
     int st = jacobi_ring(s, p, k, X, ldx, W, ldw, tol, fd, fs);
+    if (st == kUnsupported) st = jacobi_pring(s, p, k, X, ldx, W, ldw, tol, fd, fs);
     if (st == kUnsupported) st = jacobi_gring(s, p, k, X, ldx, W, ldw, tol, fd, fs);
     if (st != kUnsupported) return st;
   }

@@ -18,7 +18,9 @@ def t(f):
     torch.cuda.synchronize(); t0 = time.perf_counter(); r = f(); torch.cuda.synchronize(); return r, time.perf_counter() - t0
 dmask = T.tt_diag(system.mask)
 dkd, t1 = t(lambda: T.tt_matmat(dmask, T.tt_matmat(system.K, dmask)))
+torch.cuda.nvtx.range_push("dkd")
 k1, t2 = t(lambda: T.tt_round(dkd, eps))
+torch.cuda.nvtx.range_pop()
 ones = T.TTVector([np.ones((1, 2, 1))] * system.mask.d)
 comp = T.tt_sub(ones, system.mask)
 k2, t3 = t(lambda: T.tt_round(T.tt_add(k1, T.tt_scale(T.tt_diag(comp), system.gamma)), eps))
