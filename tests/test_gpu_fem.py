@@ -170,3 +170,28 @@ def test_variable_modulus_assembly_matches_oracle(d):
         t = getattr(got, blk)
         assert t.ranks == O.ranks(ref[blk]), (blk, t.ranks, O.ranks(ref[blk]))
         assert rel(tt_contract(t), O.full(ref[blk])) < 1e-9, blk
+
+
+@pytest.mark.parametrize("ordering,paper_det", [("canonical", False), ("canonical", True), ("zorder", True)])
+def test_general_quad_orderings_match_oracle(ordering, paper_det):
+    """Secondary API surface: canonical node ordering and
+    the paper's determinant variant on a non-parallelogram patch (general
+    element grids, assembly.py:131-158, element.py:95-100) against the
+    oracle restatement; identical ranks, dense agreement."""
+    from oracle import fem as F
+    from oracle import tt as O
+    from paper_2501_07778_b200 import assembly as A
+    from paper_2501_07778_b200.material import MaterialModel
+    from paper_2501_07778_b200.mesh import SubdomainMesh
+    from paper_2501_07778_b200.ttcore import tt_contract
+
+    quad = np.array([[0.0, 0.0], [1.2, 0.1], [1.0, 0.9], [-0.1, 1.1]])
+    mat = MaterialModel(2.0, 0.25, "plane-strain")
+    mesh = SubdomainMesh(quad, 3, {"left": "clamped"}, {"right": (0.5, -1.0)})
+    ref = F.assemble(mesh, mat, ordering, 1e-11, body=(0.3, -1.0), paper_det=paper_det)
+    got = A.assemble_subdomain(mesh, mat, ordering, 1e-11, body_force=(0.3, -1.0),
+                               paper_determinant=paper_det, cache=False)
+    for blk in ("kxx", "kxy", "kyx", "kyy"):
+        t = getattr(got, blk)
+        assert t.ranks == O.ranks(ref[blk]), (blk, t.ranks, O.ranks(ref[blk]))
+        assert rel(tt_contract(t), O.full(ref[blk])) < 1e-9, blk
