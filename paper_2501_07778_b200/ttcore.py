@@ -122,8 +122,11 @@ class _TT:
     def numpy_cores(self) -> list:
         """Host copies of the cores: one D2H copy of the packed buffer into
         pinned memory, returned as numpy views of it."""
-        host = torch.empty(self.data.numel(), dtype=torch.float64, pin_memory=True)
-        host.copy_(self.data)
+        # only the used extent: results of tt_round / tt_decompose live in
+        # input-sized buffers that can be much larger than the rounded cores
+        end = max((o + int(np.prod(s)) for o, s in zip(self._offs, self._shapes)), default=0)
+        host = torch.empty(max(end, 1), dtype=torch.float64, pin_memory=True)
+        host[:end].copy_(self.data[:end])
         hv = host.numpy()
         return [hv[o : o + int(np.prod(s))].reshape(s) for o, s in zip(self._offs, self._shapes)]
 
