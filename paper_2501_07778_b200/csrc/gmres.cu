@@ -77,20 +77,20 @@ __global__ void scale_by_kernel(int64_t n, const double* __restrict__ den, doubl
 
 // Classical Gram-Schmidt building blocks (memory bound; replace GEMV-shaped
 // GEMMs that waste 63/64 of a DMMA tile).  V is row-major (nv x dim).
-constexpr int MD_THREADS = 256, MD_E = 4, MD_CHUNK = MD_THREADS * MD_E;
+constexpr int MD_THREADS = 256, MD_E = 4;  // up to MD_E elements per thread
 
 // part[blk * nv + i] = sum over block chunk of V[i, t] * w[t]
 __global__ void __launch_bounds__(MD_THREADS) mdot_partial_kernel(int nv, int64_t dim,
                                                                   const double* __restrict__ V,
                                                                   const double* __restrict__ w,
-                                                                  double* __restrict__ part) {
+                                                                  double* __restrict__ part, int ce) {
   __shared__ double red[MD_THREADS / 32][64];
-  const int64_t base = (int64_t)blockIdx.x * MD_CHUNK + threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * MD_THREADS * ce + threadIdx.x;
   double wv[MD_E];
 #pragma unroll
   for (int e = 0; e < MD_E; ++e) {
     const int64_t t = base + e * MD_THREADS;
-    wv[e] = t < dim ? w[t] : 0.0;
+    wv[e] = (e < ce && t < dim) ? w[t] : 0.0;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = 0; i < nv; ++i) {
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(MD_THREADS) mdot_partial_kernel(int nv, int64_
 #pragma unroll
     for (int e = 0; e < MD_E; ++e) {
       const int64_t t = base + e * MD_THREADS;
-      if (t < dim) acc = fma(vi[t], wv[e], acc);
+      if (e < ce && t < dim) acc = fma(vi[t], wv[e], acc);
     }
     acc = warp_sum(acc);
     if (lane == 0) red[warp][i] = acc;
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(MD_THREADS) vcomb_kernel(int nv, int64_t dim,
                                                            const double* __restrict__ part,
                                                            int nblk, double sign, double* w,
                                                            double* __restrict__ cout,
-                                                           double* __restrict__ npart) {
+                                                           double* __restrict__ npart, int ce) {
   __shared__ double c[64];
   __shared__ double tmp[MD_THREADS / 64][64];
   __shared__ double red[MD_THREADS / 32];
@@ -143,11 +143,11 @@ __global__ void __launch_bounds__(MD_THREADS) vcomb_kernel(int nv, int64_t dim,
   }
   __syncthreads();
   double nacc = 0.0;
-  const int64_t base = (int64_t)blockIdx.x * MD_CHUNK + threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * MD_THREADS * ce + threadIdx.x;
 #pragma unroll
   for (int e = 0; e < MD_E; ++e) {
     const int64_t t = base + e * MD_THREADS;
-    if (t < dim) {
+    if (e < ce && t < dim) {
       double acc = 0.0;
       for (int i = 0; i < nv; ++i) acc = fma(V[(int64_t)i * dim + t], c[i], acc);
       const double v = fma(sign, acc, w[t]);
@@ -255,7 +255,9 @@ int local_gmres(cudaStream_t s, const LocalOp& op, const double* rhs, const doub
   *converged = 0;
   DevMem mem;
   if (restart > 63) return kInvalid;  // Hessenberg columns live in 64-entry smem
-  const int nblk = (int)ceil_div(dim, MD_CHUNK);
+  // elements per thread: enough blocks to cover the SMs at small dims
+  const int ce = dim >= (int64_t)MD_THREADS * 4 * num_sms() ? 4 : dim >= (int64_t)MD_THREADS * 2 * num_sms() ? 2 : 1;
+  const int nblk = (int)ceil_div(dim, (int64_t)MD_THREADS * ce);
   double *V, *h, *h2, *hv, *yv, *part, *npart;
   QTT_TRY(mem.get(s, &part, (int64_t)nblk * (restart + 1)));
   QTT_TRY(mem.get(s, &npart, nblk));
@@ -306,13 +308,13 @@ int local_gmres(cudaStream_t s, const LocalOp& op, const double* rhs, const doub
       QTT_TRY(local_apply(s, op, V + (int64_t)j * dim, w));
       // CGS2: h = V^T w, w -= V h (twice), then ||w|| (fused into the 2nd update)
       const int nv = j + 1;
-      mdot_partial_kernel<<<nblk, MD_THREADS, 0, s>>>(nv, dim, V, w, part);
+      mdot_partial_kernel<<<nblk, MD_THREADS, 0, s>>>(nv, dim, V, w, part, ce);
       QTT_CHECK_LAUNCH();
-      vcomb_kernel<<<nblk, MD_THREADS, 0, s>>>(nv, dim, V, part, nblk, -1.0, w, h, nullptr);
+      vcomb_kernel<<<nblk, MD_THREADS, 0, s>>>(nv, dim, V, part, nblk, -1.0, w, h, nullptr, ce);
       QTT_CHECK_LAUNCH();
-      mdot_partial_kernel<<<nblk, MD_THREADS, 0, s>>>(nv, dim, V, w, part);
+      mdot_partial_kernel<<<nblk, MD_THREADS, 0, s>>>(nv, dim, V, w, part, ce);
       QTT_CHECK_LAUNCH();
-      vcomb_kernel<<<nblk, MD_THREADS, 0, s>>>(nv, dim, V, part, nblk, -1.0, w, h2, npart);
+      vcomb_kernel<<<nblk, MD_THREADS, 0, s>>>(nv, dim, V, part, nblk, -1.0, w, h2, npart, ce);
       QTT_CHECK_LAUNCH();
       hess_col_kernel<<<1, 256, 0, s>>>(nv, h, h2, npart, nblk, hv);
       QTT_CHECK_LAUNCH();
@@ -350,7 +352,7 @@ int local_gmres(cudaStream_t s, const LocalOp& op, const double* rhs, const doub
     }
     for (int i = 0; i < jend; ++i) host[i] = y[i];
     QTT_CUDA(cudaMemcpyAsync(yv, host, sizeof(double) * jend, cudaMemcpyHostToDevice, s));
-    vcomb_kernel<<<nblk, MD_THREADS, 0, s>>>(jend, dim, V, yv, 1, 1.0, x, nullptr, nullptr);
+    vcomb_kernel<<<nblk, MD_THREADS, 0, s>>>(jend, dim, V, yv, 1, 1.0, x, nullptr, nullptr, ce);
     QTT_CHECK_LAUNCH();
     // the pinned buffer is reused by the next cycle: the H2D copy must land first
     QTT_CUDA(cudaStreamSynchronize(s));
