@@ -8,7 +8,7 @@ from paper_2501_07778_b200 import solver as S
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 10
 gsys, eps = build_system(4, d, {})
 torch.cuda.synchronize()
-cfg = S.SolverConfig(epsilon=eps, seed=0, local_solver="auto", truncation="residual", enrichment_rank=16)
+cfg = S.SolverConfig(epsilon=eps, seed=0, local_solver="auto", truncation="residual", enrichment_rank=24, local_rtol_factor=1e-3)
 pr = cProfile.Profile()
 t = time.perf_counter()
 pr.enable()
