@@ -126,6 +126,43 @@ def apply_tt_matrix(A: TTMatrix, v) -> torch.Tensor:
     return out
 
 
+def _apply_tt_to_tt(K: TTMatrix, u: TTVector) -> torch.Tensor:
+    """Dense y = K u for a TT operator and a TT vector (the dense residual
+    path of solver.py:81-103) without materialising u: the left half of the
+    cores is contracted into L[i_low, a, b] (operator rank a, vector rank b),
+    the right half into R[a, b, i_high], and y = L R is one GEMM.  Flops
+    ~ 2^(D/2) r_K r_u (r_K + r_u) per core plus 2^D r_K r_u, against
+    ~ 2^D r_K^2 per core for the dense chain over a materialised u (about 5x
+    fewer at the config-4 ranks).  Returns the flat (row-index) vector."""
+    Kc, uc = K.cores, u.cores
+    D = len(uc)
+    m = D // 2
+    dev = u.data.device
+    L = torch.ones((1, 1, 1), dtype=torch.float64, device=dev)
+    for l in range(m):
+        rk, ni, nj, rk2 = Kc[l].shape
+        ru, _, ru2 = uc[l].shape
+        P = L.shape[0]
+        T = mm(L.reshape(P * rk, ru), uc[l].reshape(ru, nj * ru2))  # (P, a, j, b')
+        T = T.view(P, rk, nj, ru2).permute(0, 3, 1, 2).reshape(P * ru2, rk * nj)
+        Kp = Kc[l].permute(0, 2, 1, 3).reshape(rk * nj, ni * rk2)  # ((a, j), (i, a'))
+        U = mm(T, Kp).view(P, ru2, ni, rk2)
+        L = U.permute(2, 0, 3, 1).reshape(ni * P, rk2, ru2)  # new bit is the slowest
+    R = torch.ones((1, 1, 1), dtype=torch.float64, device=dev)
+    for l in range(D - 1, m - 1, -1):
+        rk, ni, nj, rk2 = Kc[l].shape
+        ru, _, ru2 = uc[l].shape
+        Q = R.shape[2]
+        T = mm(uc[l].reshape(ru * nj, ru2), R.permute(1, 0, 2).reshape(ru2, rk2 * Q))  # (b, j, a', Q)
+        T = T.view(ru, nj, rk2, Q).permute(0, 3, 1, 2).reshape(ru * Q, nj * rk2)
+        Kp = Kc[l].permute(2, 3, 0, 1).reshape(nj * rk2, rk * ni)  # ((j, a'), (a, i))
+        U = mm(T, Kp).view(ru, Q, rk, ni)
+        R = U.permute(2, 0, 1, 3).reshape(rk, ru, Q * ni)  # new bit is the fastest
+    P, Q = L.shape[0], R.shape[2]
+    # y[i_low + P i_high] = sum_ab L[i_low, a, b] R[a, b, i_high]
+    return mm(R.reshape(-1, Q), L.reshape(P, -1), ta=True, tb=True).view(-1)
+
+
 def residual(K: TTMatrix, u: TTVector, f: TTVector, rounding_eps=None) -> float:
     """||K u - f|| / ||f|| (solver.py:81-103).  Dense on the device up to
     2^_DENSE_RESIDUAL_BITS entries, else in TT arithmetic with the norm taken
@@ -134,9 +171,8 @@ def residual(K: TTMatrix, u: TTVector, f: TTVector, rounding_eps=None) -> float:
     if fn == 0.0:
         return 0.0
     if len(u.cores) <= _DENSE_RESIDUAL_BITS:
-        ud = tt_contract_device(u)
         fd = tt_contract_device(f)
-        r = apply_tt_matrix(K, ud) - fd
+        r = _apply_tt_to_tt(K, u) - fd
         return float(torch.linalg.vector_norm(r) / torch.linalg.vector_norm(fd))
     y = tt_sub(tt_matvec(K, u), f)
     if rounding_eps is not None:
@@ -162,8 +198,7 @@ class _AsyncResidual:
         fd.record_stream(side)
         K.data.record_stream(side)
         with torch.cuda.stream(side):
-            ud = tt_contract_device(u)
-            r = apply_tt_matrix(K, ud) - fd
+            r = _apply_tt_to_tt(K, u) - fd
             self._val = torch.linalg.vector_norm(r) / torch.linalg.vector_norm(fd)
             self._ev = torch.cuda.Event()
             self._ev.record(side)

@@ -216,3 +216,23 @@ def test_dense_solve_kernel():
     m = np.array([[0.0, 1.0], [1.0, 0.0]])
     x, fb = dense_solve_colmajor(torch.tensor(m.T.ravel(), device="cuda"), 2, torch.tensor([1.0, 2.0], dtype=torch.float64, device="cuda"))
     assert fb and np.allclose(x.cpu().numpy(), [2.0, 1.0])
+
+
+@pytest.mark.parametrize("d,rk,ru", [(1, 1, 1), (2, 3, 2), (7, 5, 6), (12, 9, 13)])
+def test_apply_tt_to_tt_matches_dense_chain(d, rk, ru):
+    """Split left/right contraction of K u (dense residual path) equals the
+    dense chain over the materialised u (solver.apply_tt_matrix)."""
+    import torch
+
+    from paper_2501_07778_b200 import solver as S
+    from paper_2501_07778_b200 import ttcore as T
+
+    rng = np.random.default_rng(100 * d + rk)
+    ka = [1] + [rk] * (d - 1) + [1]
+    ua = [1] + [ru] * (d - 1) + [1]
+    K = T.TTMatrix([rng.standard_normal((ka[k], 2, 2, ka[k + 1])) for k in range(d)])
+    u = T.TTVector([rng.standard_normal((ua[k], 2, ua[k + 1])) for k in range(d)])
+    y = S._apply_tt_to_tt(K, u)
+    ref = S.apply_tt_matrix(K, T.tt_contract_device(u))
+    assert y.shape == ref.shape
+    assert float(torch.linalg.vector_norm(y - ref) / torch.linalg.vector_norm(ref)) < 1e-13
