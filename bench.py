@@ -219,7 +219,10 @@ def run_ours(args):
         if serial or args.serial:
             zs = [pair_job(p) for p in PAIRS]
         else:
-            zs = _lib.run_concurrent([(pair_job, p) for p in PAIRS])
+            # largest pairs first: they bound the step
+            order = sorted(PAIRS, key=lambda p: -p[0] * p[1])
+            zs = dict(zip(order, _lib.run_concurrent([(pair_job, p) for p in order])))
+            zs = [zs[p] for p in PAIRS]
         return {p: z.ranks for p, z in zip(PAIRS, zs)} if check else {}
 
     def barrier():
@@ -274,7 +277,7 @@ def run_ours(args):
             for p in PAIRS:
                 e2e_job(p)
         else:
-            _lib.run_concurrent([(e2e_job, p) for p in PAIRS])
+            _lib.run_concurrent([(e2e_job, p) for p in sorted(PAIRS, key=lambda p: -p[0] * p[1])])
         torch.cuda.synchronize()
         if s == 0:
             for p in PAIRS:

@@ -177,9 +177,9 @@ def run_concurrent(jobs):
     global _POOL, _STREAMS
     dev = torch.cuda.current_device()
     if _POOL is None:
-        _POOL = concurrent.futures.ThreadPoolExecutor(max_workers=6, thread_name_prefix="qtt-chain")
+        _POOL = concurrent.futures.ThreadPoolExecutor(max_workers=12, thread_name_prefix="qtt-chain")
     if len(_STREAMS) < len(jobs) or _STREAMS[0].device.index != dev:
-        _STREAMS = [torch.cuda.Stream(device=dev) for _ in range(max(6, len(jobs)))]
+        _STREAMS = [torch.cuda.Stream(device=dev) for _ in range(max(12, len(jobs)))]
     main = torch.cuda.current_stream()
 
     def run(fn, arg, stream):
