@@ -249,6 +249,52 @@ namespace {
 
 constexpr int TSQR_THREADS = 256;
 
+// Carry of a wide TT-SVD step: out (k x N) = U^T (k x m) C (m x N), all
+// column-major, m <= 64.  One thread per column of C (its m entries in
+// registers, U in shared memory): a single streaming pass over C, which is
+// what bounds this step (a 64-wide DMMA tile would waste 63/64 of its
+// work for k, m ~ 2..46 and run ~20x under the HBM rate).
+template <int MM>
+__global__ void __launch_bounds__(256) carry_tn_kernel(int m, int k, int64_t N,
+                                                       const double* __restrict__ U,
+                                                       const double* __restrict__ C,
+                                                       double* __restrict__ out) {
+  __shared__ double Us[64 * 64];
+  for (int idx = threadIdx.x; idx < m * k; idx += blockDim.x) Us[idx] = U[idx];
+  __syncthreads();
+  for (int64_t col = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; col < N;
+       col += (int64_t)gridDim.x * blockDim.x) {
+    const double* c = C + col * m;
+    double cv[MM];
+#pragma unroll
+    for (int j = 0; j < MM; ++j) cv[j] = j < m ? c[j] : 0.0;
+    double* o = out + col * k;
+    for (int i = 0; i < k; ++i) {
+      const double* u = Us + (int64_t)i * m;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < MM; ++j)
+        if (j < m) acc = fma(u[j], cv[j], acc);
+      o[i] = acc;
+    }
+  }
+}
+
+int carry_tn(cudaStream_t s, int m, int k, int64_t N, const double* U, const double* C, double* out) {
+  if (m > 64 || k > 64) return dgemm(s, 1, 0, k, (int)N, m, 1.0, U, m, C, m, 0.0, out, k);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(N, 256), 16 * num_sms()));
+  if (m <= 8)
+    carry_tn_kernel<8><<<grid, 256, 0, s>>>(m, k, N, U, C, out);
+  else if (m <= 16)
+    carry_tn_kernel<16><<<grid, 256, 0, s>>>(m, k, N, U, C, out);
+  else if (m <= 32)
+    carry_tn_kernel<32><<<grid, 256, 0, s>>>(m, k, N, U, C, out);
+  else
+    carry_tn_kernel<64><<<grid, 256, 0, s>>>(m, k, N, U, C, out);
+  QTT_CHECK_LAUNCH();
+  return kOk;
+}
+
 // R factor (upper m x m, row-major into the stack) of a BR x m block of the
 // row-major tall matrix src (rows x m).  Unblocked Householder in smem.
 __global__ void __launch_bounds__(TSQR_THREADS) tsqr_leaf_kernel(int64_t rows, int m, int br,
@@ -433,7 +479,7 @@ int decompose(const double* dense, int d, const int64_t* sizes, double eps, qtt_
       QTT_TRY(Ub.alloc(s, (int64_t)m * newk));
       QTT_TRY(gather_columns(s, m, newk, W.p, m, perm, Ub.p, m));
       QTT_TRY(nxt.alloc(s, (int64_t)newk * N));
-      QTT_TRY(dgemm(s, 1, 0, newk, (int)N, m, 1.0, Ub.p, m, cur, m, 0.0, nxt.p, newk));
+      QTT_TRY(carry_tn(s, m, newk, N, Ub.p, cur, nxt.p));
     } else {
       // tall (or too wide for TSQR): C (m x N) column-major; QR then Jacobi on R^T
       const int kk = (int)std::min<int64_t>(m, N);
