@@ -11,6 +11,7 @@
 // the solve falls back to Householder QR (backward stable, ~2x the flops).
 #include "../../include/qtt_b200.h"
 #include <cmath>
+#include <cstdlib>
 
 #include "linalg.cuh"
 
@@ -115,6 +116,12 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
   QTT_CUDA(cudaMallocAsync(&Up, sizeof(double) * (int64_t)LB * (N + 1), s));
   lu_diag_kernel<<<1, 256, kLuSmem, s>>>(std::min(LB, N), A, ld, linv, uinv, bad);
   QTT_CHECK_LAUNCH();
+  // Two-level blocking for large N: block pairs (a, b) share ONE trailing
+  // update with K = 128 (a's update of the rows below b is deferred to b),
+  // which runs the Schur complement GEMM at a higher DMMA efficiency than
+  // two K = 64 updates; the look-ahead of the next diagonal block is kept.
+  static const bool two_level_env = getenv("QTT_LU_ONE_LEVEL") == nullptr;
+  const bool two_level = two_level_env && N >= 2048;
   for (int kb0 = 0, blk = 0; kb0 < N; kb0 += LB, ++blk) {
     const int kb = std::min(LB, N - kb0);
     const int m2 = N - kb0 - kb;      // rows below
@@ -125,25 +132,48 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
       QTT_TRY(dgemm(s, 0, 0, m2, kb, kb, 1.0, A21, ld, uinv + (int64_t)blk * LB * LB, LB, 0.0, Lp, m2));
     // U12 = L11^{-1} A12 (includes the rhs column)
     QTT_TRY(dgemm(s, 0, 0, kb, n2, kb, 1.0, linv + (int64_t)blk * LB * LB, LB, A12, ld, 0.0, Up, kb));
-    const int kb1 = m2 > 0 ? std::min(LB, m2) : 0;
-    if (kb1 > 0) {
-      double* A22n = A + (kb0 + kb) + (int64_t)(kb0 + kb) * ld;  // next block column
-      QTT_TRY(dgemm(s, 0, 0, m2, kb1, kb, -1.0, Lp, m2, Up, kb, 1.0, A22n, ld));
-      QTT_CUDA(cudaEventRecord(ev_col, s));
-      QTT_CUDA(cudaStreamWaitEvent(sb, ev_col, 0));
-      lu_diag_kernel<<<1, 256, kLuSmem, sb>>>(kb1, A22n, ld, linv + (int64_t)(blk + 1) * LB * LB,
-                                              uinv + (int64_t)(blk + 1) * LB * LB, bad);
-      QTT_CHECK_LAUNCH();
-      QTT_CUDA(cudaEventRecord(ev_diag, sb));
-      const int rest = n2 - kb1;
-      if (rest > 0)
-        QTT_TRY(dgemm(s, 0, 0, m2, rest, kb, -1.0, Lp, m2, Up + (int64_t)kb1 * kb, kb, 1.0,
-                      A22n + (int64_t)kb1 * ld, ld));
-    }
-    // keep L21 / U12 in A for the back substitution and the refinement
+    // keep L21 / U12 in A for the paired update, the back substitution and the refinement
     if (m2 > 0) QTT_TRY(copy_matrix(s, m2, kb, Lp, m2, A21, ld));
     QTT_TRY(copy_matrix(s, kb, n2, Up, kb, A12, ld));
-    if (kb1 > 0) QTT_CUDA(cudaStreamWaitEvent(s, ev_diag, 0));
+    const int kb1 = m2 > 0 ? std::min(LB, m2) : 0;
+    const bool pair_a = two_level && (blk % 2 == 0) && kb1 > 0;
+    const bool pair_b = two_level && (blk % 2 == 1);
+    if (kb1 > 0) {
+      double* A22n = A + (kb0 + kb) + (int64_t)(kb0 + kb) * ld;  // next block column
+      const int rest = n2 - kb1;
+      if (pair_b) {
+        // both blocks of the pair (a = previous, b = this) at once, K = LB + kb
+        const int k0 = kb0 - LB, KK = LB + kb;
+        const double* Lab = A + (kb0 + kb) + (int64_t)k0 * ld;  // rows below b, cols a..b
+        const double* Uab = A + k0 + (int64_t)(kb0 + kb) * ld;  // rows a..b, cols right of b
+        QTT_TRY(dgemm(s, 0, 0, m2, kb1, KK, -1.0, Lab, ld, Uab, ld, 1.0, A22n, ld));
+        QTT_CUDA(cudaEventRecord(ev_col, s));
+        QTT_CUDA(cudaStreamWaitEvent(sb, ev_col, 0));
+        lu_diag_kernel<<<1, 256, kLuSmem, sb>>>(kb1, A22n, ld, linv + (int64_t)(blk + 1) * LB * LB,
+                                                uinv + (int64_t)(blk + 1) * LB * LB, bad);
+        QTT_CHECK_LAUNCH();
+        QTT_CUDA(cudaEventRecord(ev_diag, sb));
+        if (rest > 0)
+          QTT_TRY(dgemm(s, 0, 0, m2, rest, KK, -1.0, Lab, ld, Uab + (int64_t)kb1 * ld, ld, 1.0,
+                        A22n + (int64_t)kb1 * ld, ld));
+      } else {
+        QTT_TRY(dgemm(s, 0, 0, m2, kb1, kb, -1.0, Lp, m2, Up, kb, 1.0, A22n, ld));
+        QTT_CUDA(cudaEventRecord(ev_col, s));
+        QTT_CUDA(cudaStreamWaitEvent(sb, ev_col, 0));
+        lu_diag_kernel<<<1, 256, kLuSmem, sb>>>(kb1, A22n, ld, linv + (int64_t)(blk + 1) * LB * LB,
+                                                uinv + (int64_t)(blk + 1) * LB * LB, bad);
+        QTT_CHECK_LAUNCH();
+        QTT_CUDA(cudaEventRecord(ev_diag, sb));
+        if (rest > 0) {
+          // pair_a: only the partner's rows (needed for its U12); the rows
+          // below the partner are updated together with it
+          const int rows = pair_a ? kb1 : m2;
+          QTT_TRY(dgemm(s, 0, 0, rows, rest, kb, -1.0, Lp, m2, Up + (int64_t)kb1 * kb, kb, 1.0,
+                        A22n + (int64_t)kb1 * ld, ld));
+        }
+      }
+      QTT_CUDA(cudaStreamWaitEvent(s, ev_diag, 0));
+    }
   }
   QTT_CUDA(cudaFreeAsync(Lp, s));
   QTT_CUDA(cudaFreeAsync(Up, s));
