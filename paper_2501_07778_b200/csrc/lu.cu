@@ -105,10 +105,14 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
   // solves of block k only the next block column is updated, the next
   // diagonal block is factorised on the side stream while the rest of the
   // Schur complement is updated here.
-  thread_local cudaEvent_t ev_col = nullptr, ev_diag = nullptr;
+  thread_local cudaEvent_t ev_col = nullptr, ev_diag = nullptr, ev_fork = nullptr, ev_join = nullptr;
+  thread_local cudaStream_t su = nullptr;
   if (!ev_col) {
     QTT_CUDA(cudaEventCreateWithFlags(&ev_col, cudaEventDisableTiming));
     QTT_CUDA(cudaEventCreateWithFlags(&ev_diag, cudaEventDisableTiming));
+    QTT_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    QTT_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    QTT_CUDA(cudaStreamCreateWithFlags(&su, cudaStreamNonBlocking));
   }
   cudaStream_t sb = side_stream();
   double *Lp, *Up;
@@ -128,13 +132,20 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
     const int n2 = N + 1 - kb0 - kb;  // columns right (incl. rhs)
     double* A21 = A + (kb0 + kb) + (int64_t)kb0 * ld;
     double* A12 = A + kb0 + (int64_t)(kb0 + kb) * ld;
-    if (m2 > 0)  // L21 = A21 U11^{-1}
+    // the two panel solves are independent: U12 on a second stream while
+    // L21 runs here (both feed the next block-column update)
+    QTT_CUDA(cudaEventRecord(ev_fork, s));
+    QTT_CUDA(cudaStreamWaitEvent(su, ev_fork, 0));
+    // U12 = L11^{-1} A12 (includes the rhs column); kept in A for the paired
+    // update, the back substitution and the refinement
+    QTT_TRY(dgemm(su, 0, 0, kb, n2, kb, 1.0, linv + (int64_t)blk * LB * LB, LB, A12, ld, 0.0, Up, kb));
+    QTT_TRY(copy_matrix(su, kb, n2, Up, kb, A12, ld));
+    QTT_CUDA(cudaEventRecord(ev_join, su));
+    if (m2 > 0) {  // L21 = A21 U11^{-1}
       QTT_TRY(dgemm(s, 0, 0, m2, kb, kb, 1.0, A21, ld, uinv + (int64_t)blk * LB * LB, LB, 0.0, Lp, m2));
-    // U12 = L11^{-1} A12 (includes the rhs column)
-    QTT_TRY(dgemm(s, 0, 0, kb, n2, kb, 1.0, linv + (int64_t)blk * LB * LB, LB, A12, ld, 0.0, Up, kb));
-    // keep L21 / U12 in A for the paired update, the back substitution and the refinement
-    if (m2 > 0) QTT_TRY(copy_matrix(s, m2, kb, Lp, m2, A21, ld));
-    QTT_TRY(copy_matrix(s, kb, n2, Up, kb, A12, ld));
+      QTT_TRY(copy_matrix(s, m2, kb, Lp, m2, A21, ld));
+    }
+    QTT_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
     const int kb1 = m2 > 0 ? std::min(LB, m2) : 0;
     const bool pair_a = two_level && (blk % 2 == 0) && kb1 > 0;
     const bool pair_b = two_level && (blk % 2 == 1);
