@@ -391,6 +391,10 @@ def run_ours(args):
                 "frac": round(mv_bytes / (min(mv_ms) * 1e-3) / 1e9 / peaks["hbm_gbs"], 4)
                 if peaks.get("hbm_gbs") else None,
                 "pair": "16x128",
+                # dram__bytes_read.sum + dram__bytes_write.sum of one launch
+                # (ncu --set full, profiles/r01_summary.md): 5.98 MB + 1.416 GB
+                "traffic": 1.4225e9,
+                "algorithmic_bytes": mv_bytes,
             },
             "clocks": clk,
             "solve_wall_s": None if not extras else {
