@@ -294,7 +294,10 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel (DMMA GEMM) from per-launch events
     barrier()
-    # clean serial step (the GEMM share below is relative to it)
+    # clean serial step (the GEMM share below is relative to it); one untimed
+    # serial pass first so the main stream's allocator pool is warm
+    one_step(serial=True)
+    torch.cuda.synchronize()
     flush.zero_()
     barrier()
     es0 = torch.cuda.Event(enable_timing=True)

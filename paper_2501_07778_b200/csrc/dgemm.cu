@@ -9,6 +9,8 @@
 // AMEn environment contractions and the dense residual.
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace qtt {
 namespace {
 
@@ -27,6 +29,10 @@ struct TileCfg {
 // 128 x 64, 64 x 128, 128 x 128 and 64 x 32 tiles with 4-8 warps: none is
 // faster once the tile loads are hoisted; 8192^3 runs at cuBLAS speed.)
 using CfgSmall = TileCfg<2, 2, 4, 4, 4>;
+// 32 x 32 CTA tile (2 x 2 warps of 16 x 16) for small outputs with a short
+// reduction, where the 64 x 64 grid leaves most SMs idle and split-K does
+// not apply (k < 512).
+using CfgTiny = TileCfg<2, 2, 2, 2, 4>;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -340,7 +346,10 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
     QTT_CHECK_LAUNCH();
     return kOk;
   }
-  const int BM = CfgSmall::BM, BN = CfgSmall::BN;
+  static const bool tiny_ok = getenv("QTT_GEMM_NO_TINY") == nullptr;
+  const int64_t tiles64 = ceil_div(g.m, CfgSmall::BM) * ceil_div(g.n, CfgSmall::BN);
+  const bool tiny = tiny_ok && tiles64 * g.batch < num_sms() && g.k < 512;
+  const int BM = tiny ? CfgTiny::BM : CfgSmall::BM, BN = tiny ? CfgTiny::BN : CfgSmall::BN;
   const int mt = (int)ceil_div(g.m, BM);
   const int64_t tiles = (int64_t)mt * ceil_div(g.n, BN);
   if (tiles > 0x7fffffff) return kUnsupported;
@@ -357,7 +366,7 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
   // are reduced in a fixed order, so results stay deterministic.
   int splits = 1;
   const int64_t ctas = tiles * g.batch;
-  if (ctas < num_sms() && g.k >= 512) {
+  if (!tiny && ctas < num_sms() && g.k >= 512) {
     splits = (int)std::min<int64_t>({16, ceil_div(2 * num_sms(), ctas), g.k / 256});
     splits = std::max(splits, 1);
   }
@@ -373,6 +382,7 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
   QTT_CUDA(cudaFuncSetAttribute(gemm_kernel<TA_, TB_, CF>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                 CF::SMEM));
     QTT_CFG_ATTR(0, 0, CfgSmall) QTT_CFG_ATTR(0, 1, CfgSmall) QTT_CFG_ATTR(1, 0, CfgSmall) QTT_CFG_ATTR(1, 1, CfgSmall)
+    QTT_CFG_ATTR(0, 0, CfgTiny) QTT_CFG_ATTR(0, 1, CfgTiny) QTT_CFG_ATTR(1, 0, CfgTiny) QTT_CFG_ATTR(1, 1, CfgTiny)
 #undef QTT_CFG_ATTR
     configured = true;
   }
@@ -383,7 +393,10 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
     else if (g.trans_a && !g.trans_b) gemm_kernel<1, 0, CF><<<grid, CF::THREADS, CF::SMEM, stream>>>(g, mt, kchunk, ws); \
     else gemm_kernel<1, 1, CF><<<grid, CF::THREADS, CF::SMEM, stream>>>(g, mt, kchunk, ws);       \
   } while (0)
-  QTT_LAUNCH(CfgSmall);
+  if (tiny)
+    QTT_LAUNCH(CfgTiny);
+  else
+    QTT_LAUNCH(CfgSmall);
 #undef QTT_LAUNCH
   QTT_CHECK_LAUNCH();
   if (splits > 1) {
