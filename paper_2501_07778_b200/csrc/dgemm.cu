@@ -364,8 +364,16 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
   // Split K when the tile grid cannot fill the SMs (skinny outputs with a
   // long reduction, e.g. V^T A in the compact-WY updates); the partial sums
   // are reduced in a fixed order, so results stay deterministic.
+  // kGemmUpperC grids count only the tiles that compute (the strictly lower
+  // ones exit at once), so a Gram matrix with a long reduction splits too.
   int splits = 1;
-  const int64_t ctas = tiles * g.batch;
+  int64_t work_tiles = tiles;
+  if (g.flags & kGemmUpperC) {
+    const int64_t nt = ceil_div(g.n, BN);
+    work_tiles = 0;
+    for (int64_t ni = 0; ni < nt; ++ni) work_tiles += std::min<int64_t>(mt, ceil_div((ni + 1) * BN, BM));
+  }
+  const int64_t ctas = work_tiles * g.batch;
   if (!tiny && ctas < num_sms() && g.k >= 512) {
     splits = (int)std::min<int64_t>({16, ceil_div(2 * num_sms(), ctas), g.k / 256});
     splits = std::max(splits, 1);

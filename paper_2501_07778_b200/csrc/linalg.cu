@@ -1763,19 +1763,21 @@ int tri_inverse(cudaStream_t s, int k, const double* R, int64_t ldr, double* X) 
   // Recursive doubling: X12 = -X11 * R12 * X22 for block pairs of size sz.
   // All full pairs of a level have the same shape and a constant stride
   // 2 sz (1 + ld) along the diagonal: one batched GEMM per product and level;
-  // a trailing partial pair (c < sz) is issued separately.
+  // a trailing partial pair (c < sz) is issued separately.  X22 and X11 are
+  // upper triangular, so each tile's reduction is clipped to their nonzeros
+  // (kGemmTriB / kGemmTriA: half the flops, bitwise the same result).
   for (int sz = TRB; sz < k; sz *= 2) {
     const int full = (k / (2 * sz));  // pairs with c == sz
     if (full > 0) {
       GemmArgs g1{sz, sz, sz, 0, 0, 1.0, 0.0,
                   R + (int64_t)sz * ldr, ldr, 2 * (int64_t)sz * (1 + ldr),
                   X + sz + (int64_t)sz * kk, kk, 2 * (int64_t)sz * (1 + kk),
-                  T, sz, (int64_t)sz * sz, full};
+                  T, sz, (int64_t)sz * sz, full, kGemmTriB};
       QTT_TRY(gemm(g1, s));
       GemmArgs g2{sz, sz, sz, 0, 0, -1.0, 0.0,
                   X, kk, 2 * (int64_t)sz * (1 + kk),
                   T, sz, (int64_t)sz * sz,
-                  X + (int64_t)sz * kk, kk, 2 * (int64_t)sz * (1 + kk), full};
+                  X + (int64_t)sz * kk, kk, 2 * (int64_t)sz * (1 + kk), full, kGemmTriA};
       QTT_TRY(gemm(g2, s));
     }
     const int b = full * 2 * sz;
@@ -1785,8 +1787,8 @@ int tri_inverse(cudaStream_t s, int k, const double* R, int64_t ldr, double* X) 
       const double* X22 = X + (b + sz) + (int64_t)(b + sz) * kk;
       const double* X11 = X + b + (int64_t)b * kk;
       double* X12 = X + b + (int64_t)(b + sz) * kk;
-      QTT_TRY(dgemm(s, 0, 0, sz, c, c, 1.0, R12, ldr, X22, kk, 0.0, T, sz));
-      QTT_TRY(dgemm(s, 0, 0, sz, c, sz, -1.0, X11, kk, T, sz, 0.0, X12, kk));
+      QTT_TRY(dgemm(s, 0, 0, sz, c, c, 1.0, R12, ldr, X22, kk, 0.0, T, sz, kGemmTriB));
+      QTT_TRY(dgemm(s, 0, 0, sz, c, sz, -1.0, X11, kk, T, sz, 0.0, X12, kk, kGemmTriA));
     }
   }
   QTT_CUDA(cudaFreeAsync(T, s));
