@@ -66,8 +66,14 @@ __global__ void __launch_bounds__(Cfg::THREADS) gemm_kernel(GemmArgs g, int mt, 
   const int first_m = (tile / (GROUP * nt)) * GROUP;
   const int gsz = min(mt - first_m, GROUP);
   const int in_group = tile % (GROUP * nt);
-  const int m0 = (first_m + in_group % gsz) * BM;
-  const int n0 = (in_group / gsz) * BN;
+  int mi = first_m + in_group % gsz, ni = in_group / gsz;
+  // Triangular operands make tiles unequal: issue the longest reductions
+  // first (kGemmTriB / kGemmLowA: K grows with n / m) so they do not form
+  // the tail of the last wave.
+  if (g.flags & kGemmTriB) ni = nt - 1 - ni;
+  if (g.flags & kGemmLowA) mi = mt - 1 - mi;
+  const int m0 = mi * BM;
+  const int n0 = ni * BN;
   const int bz = blockIdx.y;
   const double* A = g.a + bz * g.stride_a;
   const double* B = g.b + bz * g.stride_b;
