@@ -197,6 +197,14 @@ int qtt_gemm(int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,
              int64_t k, double alpha, const double* a, int64_t lda,
              const double* b, int64_t ldb, double beta, double* c,
              int64_t ldc, void* stream);
+/* qtt_gemm with the internal structure flags of the rounding/Cholesky
+ * products (bit 1: only the upper-triangular 64x64 tiles of C are computed;
+ * 2 / 4: op(A) / op(B) upper triangular; 8 / 16: lower triangular), so the
+ * parity tests reach the clipped-reduction, split-K and tile-order paths. */
+int qtt_gemm_structured(int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,
+                        int64_t k, double alpha, const double* a, int64_t lda,
+                        const double* b, int64_t ldb, double beta, double* c,
+                        int64_t ldc, int32_t flags, void* stream);
 /* Householder QR of a column-major m x n matrix: Q (m x k), R (k x n). */
 int qtt_qr(int64_t m, int64_t n, const double* a, int64_t lda, double* q,
            int64_t ldq, double* r, int64_t ldr, void* stream);

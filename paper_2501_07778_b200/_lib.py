@@ -50,6 +50,7 @@ EXPORTS = (
     "qtt_local_gmres",
     "qtt_local_apply",
     "qtt_gemm",
+    "qtt_gemm_structured",
     "qtt_qr",
     "qtt_svd",
 )

@@ -250,6 +250,17 @@ int qtt_gemm(int32_t trans_a, int32_t trans_b, int64_t m, int64_t n, int64_t k, 
                ldc);
 }
 
+int qtt_gemm_structured(int32_t trans_a, int32_t trans_b, int64_t m, int64_t n, int64_t k,
+                        double alpha, const double* a, int64_t lda, const double* b, int64_t ldb,
+                        double beta, double* c, int64_t ldc, int32_t flags, void* stream) {
+  pool_init();
+  if (m < 0 || n < 0 || k < 0 || m > 0x7fffffff || n > 0x7fffffff || k > 0x7fffffff ||
+      (flags & ~31) != 0)
+    return QTT_EINVAL;
+  return dgemm(S(stream), trans_a, trans_b, (int)m, (int)n, (int)k, alpha, a, lda, b, ldb, beta, c,
+               ldc, flags);
+}
+
 int qtt_qr(int64_t m, int64_t n, const double* a, int64_t lda, double* q, int64_t ldq, double* r,
            int64_t ldr, void* stream) {
   pool_init();

@@ -48,6 +48,53 @@ def test_gemm_all_transposes():
             assert np.abs(got - want).max() < 1e-12 * np.abs(want).max()
 
 
+@pytest.mark.parametrize(
+    "m,n,k,ta,flags",
+    [
+        (64, 64, 64, 0, 2 | 4),          # 32x32 tiles, both operands upper triangular
+        (512, 512, 512, 0, 4),           # split-K, B upper (tri-inverse level)
+        (512, 512, 512, 0, 2),           # split-K, A upper
+        (1024, 1024, 4096, 1, 1),        # upper-C Gram, split over the computing tiles only
+        (2048, 2048, 2048, 0, 2 | 4),    # longest-reduction-first tile order
+        (1000, 1000, 1000, 0, 1 | 8 | 4),  # upper C, A lower, B upper, ragged tiles
+        (700, 300, 700, 0, 16),          # B lower triangular
+    ],
+)
+def test_gemm_structured(m, n, k, ta, flags):
+    """Structure-flagged DMMA GEMM (upper-C tiles, triangular operand
+    clipping, split-K, tile order) against the dense float64 product."""
+    rng = np.random.default_rng(m + 7 * n + k + flags)
+    a = rng.standard_normal((k, m) if ta else (m, k))
+    b = rng.standard_normal((k, n))
+    opa = a.T if ta else a
+    if flags & 2:
+        opa = np.triu(opa)
+    if flags & 8:
+        opa = np.tril(opa)
+    a = opa.T if ta else opa
+    if flags & 4:
+        b = np.triu(b)
+    if flags & 16:
+        b = np.tril(b)
+    c0 = rng.standard_normal((m, n))
+    A = torch.tensor(np.asfortranarray(a).ravel(order="F"), device="cuda")
+    B = torch.tensor(np.asfortranarray(b).ravel(order="F"), device="cuda")
+    C = torch.tensor(c0.ravel(order="F"), device="cuda")
+    from paper_2501_07778_b200 import _lib
+    import ctypes
+
+    _lib.call("qtt_gemm_structured", ctypes.c_int32(ta), ctypes.c_int32(0), ctypes.c_int64(m),
+              ctypes.c_int64(n), ctypes.c_int64(k), ctypes.c_double(-0.5), _lib.ptr(A),
+              ctypes.c_int64(a.shape[0]), _lib.ptr(B), ctypes.c_int64(k), ctypes.c_double(1.5),
+              _lib.ptr(C), ctypes.c_int64(m), ctypes.c_int32(flags), _lib.stream_handle())
+    want = -0.5 * opa @ b + 1.5 * c0
+    got = C.cpu().numpy().reshape((n, m)).T
+    if flags & 1:  # only the upper triangle (incl. diagonal) is specified
+        mask = np.triu(np.ones((m, n), dtype=bool))
+        got, want = got[mask], want[mask]
+    assert np.abs(got - want).max() < 1e-12 * np.sqrt(k) * np.abs(want).max()
+
+
 @pytest.mark.parametrize("m,n", [(5, 3), (64, 64), (300, 40), (100, 150), (2000, 96), (4100, 70),
                                  (128, 64), (768, 20), (20, 60), (400, 64), (1, 7), (33, 1)])
 def test_qr_explicit(m, n):
