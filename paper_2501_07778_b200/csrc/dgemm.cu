@@ -30,8 +30,9 @@ struct TileCfg {
 // faster once the tile loads are hoisted; 8192^3 runs at cuBLAS speed.)
 using CfgSmall = TileCfg<2, 2, 4, 4, 4>;
 // 32 x 32 CTA tile (2 x 2 warps of 16 x 16) for small outputs with a short
-// reduction, where the 64 x 64 grid leaves most SMs idle and split-K does
-// not apply (k < 512).
+// reduction (k < 1024; QTT_GEMM_TINY_K overrides), where the 64 x 64 grid
+// leaves most SMs idle: 4x the CTAs beats a 2-way split-K at k = 512-768
+// (tools/tiny_ab.py; config-2 serial step 148 -> 145 ms).
 using CfgTiny = TileCfg<2, 2, 2, 2, 4>;
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
@@ -354,7 +355,8 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
   }
   static const bool tiny_ok = getenv("QTT_GEMM_NO_TINY") == nullptr;
   const int64_t tiles64 = ceil_div(g.m, CfgSmall::BM) * ceil_div(g.n, CfgSmall::BN);
-  const bool tiny = tiny_ok && tiles64 * g.batch < num_sms() && g.k < 512;
+  static const int tiny_k = getenv("QTT_GEMM_TINY_K") ? atoi(getenv("QTT_GEMM_TINY_K")) : 1024;
+  const bool tiny = tiny_ok && tiles64 * g.batch < num_sms() && g.k < tiny_k;
   const int BM = tiny ? CfgTiny::BM : CfgSmall::BM, BN = tiny ? CfgTiny::BN : CfgSmall::BN;
   const int mt = (int)ceil_div(g.m, BM);
   const int64_t tiles = (int64_t)mt * ceil_div(g.n, BN);
