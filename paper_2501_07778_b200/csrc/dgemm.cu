@@ -382,8 +382,9 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
     for (int64_t ni = 0; ni < nt; ++ni) work_tiles += std::min<int64_t>(mt, ceil_div((ni + 1) * BN, BM));
   }
   const int64_t ctas = work_tiles * g.batch;
-  if (!tiny && ctas < num_sms() && g.k >= 512) {
-    splits = (int)std::min<int64_t>({16, ceil_div(2 * num_sms(), ctas), g.k / 256});
+  static const int split_fill = getenv("QTT_GEMM_SPLIT_FILL") ? atoi(getenv("QTT_GEMM_SPLIT_FILL")) : 1;
+  if (!tiny && ctas < split_fill * num_sms() && g.k >= 512) {
+    splits = (int)std::min<int64_t>({16, ceil_div((split_fill + 1) * num_sms(), ctas), g.k / 256});
     splits = std::max(splits, 1);
   }
   const int kchunk = splits > 1 ? (int)(ceil_div(ceil_div(g.k, splits), BK) * BK) : g.k;
