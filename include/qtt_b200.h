@@ -63,6 +63,10 @@ long long qtt_launch_count(void);
  * algorithmic FLOPs (2mnk), the summed event time and the launch count. */
 int qtt_profile_gemm(int32_t on);
 int qtt_profile_gemm_read(double* flops, double* ms, int64_t* launches);
+/* Dispatch record of the i-th profiled GEMM launch (negative i counts from
+ * the end): out[7] = {m, n, k, batch, flags, k-splits, tile rows BM}.  Lets
+ * the parity tests assert which kernel configuration a shape reached. */
+int qtt_profile_gemm_shape(int64_t i, int64_t* out);
 
 /* Number of doubles a packed buffer for `lay` needs (with alignment). */
 int64_t qtt_layout_size(const qtt_layout* lay);
@@ -198,7 +202,9 @@ int qtt_gemm(int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,
              const double* b, int64_t ldb, double beta, double* c,
              int64_t ldc, void* stream);
 /* qtt_gemm with the internal structure flags of the rounding/Cholesky
- * products (bit 1: only the upper-triangular 64x64 tiles of C are computed;
+ * products (bit 1: only entries of C with row <= col are defined -- tiles entirely
+ * below the diagonal are skipped, so strictly-lower entries of diagonal
+ * tiles may be left unwritten;
  * 2 / 4: op(A) / op(B) upper triangular; 8 / 16: lower triangular), so the
  * parity tests reach the clipped-reduction, split-K and tile-order paths. */
 int qtt_gemm_structured(int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,

@@ -26,6 +26,7 @@ EXPORTS = (
     "qtt_launch_count",
     "qtt_profile_gemm",
     "qtt_profile_gemm_read",
+    "qtt_profile_gemm_shape",
     "qtt_layout_size",
     "qtt_release_cached",
     "qtt_matvec",
@@ -165,6 +166,17 @@ def gemm_profile_stop() -> tuple:
     return f.value, ms.value, n.value
 
 
+def gemm_profile_shapes(count: int) -> list:
+    """Dispatch records of the last ``count`` profiled GEMM launches, each a
+    dict (m, n, k, batch, flags, splits, bm); call before gemm_profile_stop."""
+    out = []
+    buf = (ctypes.c_int64 * 7)()
+    for i in range(-count, 0):
+        call("qtt_profile_gemm_shape", ctypes.c_int64(i), buf)
+        out.append(dict(zip(("m", "n", "k", "batch", "flags", "splits", "bm"), list(buf))))
+    return out
+
+
 _POOL = None
 _STREAMS: list = []
 
@@ -195,7 +207,11 @@ def run_concurrent(jobs):
         return out
 
     futs = [_POOL.submit(run, fn, arg, _STREAMS[i]) for i, (fn, arg) in enumerate(jobs)]
-    outs = [f.result() for f in futs]
-    for i in range(len(jobs)):
-        main.wait_stream(_STREAMS[i])
-    return outs
+    # wait for EVERY chain before joining the streams: if one job raises, the
+    # others must not keep reading or writing memory the caller may free
+    concurrent.futures.wait(futs)
+    try:
+        return [f.result() for f in futs]
+    finally:
+        for i in range(len(jobs)):
+            main.wait_stream(_STREAMS[i])

@@ -78,6 +78,7 @@ long long qtt_launch_count(void) { return g_launches.load(); }
 int qtt_profile_gemm(int32_t on) {
   pool_init();
   GemmProfile& p = gemm_profile();
+  std::lock_guard<std::mutex> lk(p.mu);
   for (auto& e : p.events) {
     cudaEventDestroy(e.first);
     cudaEventDestroy(e.second);
@@ -93,6 +94,7 @@ int qtt_profile_gemm(int32_t on) {
 int qtt_profile_gemm_read(double* flops, double* ms, int64_t* launches) {
   pool_init();
   GemmProfile& p = gemm_profile();
+  std::lock_guard<std::mutex> lk(p.mu);
   double tot = 0.0;
   for (auto& e : p.events) {
     QTT_CUDA(cudaEventSynchronize(e.second));
@@ -111,6 +113,15 @@ int qtt_profile_gemm_read(double* flops, double* ms, int64_t* launches) {
   *flops = p.flops;
   *ms = tot;
   *launches = (int64_t)p.events.size();
+  return QTT_OK;
+}
+
+int qtt_profile_gemm_shape(int64_t i, int64_t* out) {
+  GemmProfile& p = gemm_profile();
+  std::lock_guard<std::mutex> lk(p.mu);
+  if (i < 0) i += (int64_t)p.shapes.size();
+  if (i < 0 || i >= (int64_t)p.shapes.size()) return QTT_EINVAL;
+  for (int j = 0; j < 7; ++j) out[j] = p.shapes[i][j];
   return QTT_OK;
 }
 

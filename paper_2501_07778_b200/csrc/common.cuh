@@ -8,6 +8,8 @@
 #include <utility>
 #include <array>
 #include <vector>
+#include <atomic>
+#include <mutex>
 
 namespace qtt {
 
@@ -58,16 +60,34 @@ __host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) {
   return (a + b - 1) / b;
 }
 
+// SM count of the current device (cached per device; thread-safe).
 inline int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
 }
+
+// Per-device "done" flag for one-time setup such as cudaFuncSetAttribute
+// (a per-device property).  Atomic, so concurrent first calls from several
+// host threads are well defined (at worst the idempotent setup runs twice).
+struct DeviceFlag {
+  std::atomic<uint64_t> bits{0};
+  static int cur() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & 63;
+  }
+  bool test() const { return (bits.load(std::memory_order_acquire) >> cur()) & 1ull; }
+  void set() { bits.fetch_or(1ull << cur(), std::memory_order_release); }
+};
 
 // ------------------------------------------------- 64 x 64 register blocks
 // The diagonal-block kernels of the blocked Cholesky / LU / triangular
@@ -258,11 +278,12 @@ void pool_init();
 // Optional per-launch GEMM timing (CUDA events on the launching stream) used
 // by bench.py to report the DMMA kernel's achieved FLOP rate.
 struct GemmProfile {
-  bool on = false;
+  std::mutex mu;  // chains on several host threads may record concurrently
+  std::atomic<bool> on{false};
   double flops = 0.0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> events;
   std::vector<double> launch_flops;
-  std::vector<std::array<int64_t, 6>> shapes;  // m, n, k, batch, flags, splits
+  std::vector<std::array<int64_t, 7>> shapes;  // m, n, k, batch, flags, splits, tile BM
 };
 GemmProfile& gemm_profile();
 

@@ -393,15 +393,15 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
   if (splits > 1)
     QTT_CUDA(cudaMallocAsync(&ws, sizeof(double) * splits * g.batch * (int64_t)g.m * g.n, stream));
   grid.z = splits;
-  static bool configured = false;
-  if (!configured) {
+  static DeviceFlag configured;
+  if (!configured.test()) {
 #define QTT_CFG_ATTR(TA_, TB_, CF)                                                                   \
   QTT_CUDA(cudaFuncSetAttribute(gemm_kernel<TA_, TB_, CF>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                                 CF::SMEM));
     QTT_CFG_ATTR(0, 0, CfgSmall) QTT_CFG_ATTR(0, 1, CfgSmall) QTT_CFG_ATTR(1, 0, CfgSmall) QTT_CFG_ATTR(1, 1, CfgSmall)
     QTT_CFG_ATTR(0, 0, CfgTiny) QTT_CFG_ATTR(0, 1, CfgTiny) QTT_CFG_ATTR(1, 0, CfgTiny) QTT_CFG_ATTR(1, 1, CfgTiny)
 #undef QTT_CFG_ATTR
-    configured = true;
+    configured.set();
   }
 #define QTT_LAUNCH(CF)                                                                             \
   do {                                                                                             \
@@ -423,8 +423,9 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
     QTT_CHECK_LAUNCH();
     QTT_CUDA(cudaFreeAsync(ws, stream));
   }
-  if (prof.on) {
+  if (e0) {
     QTT_CUDA(cudaEventRecord(e1, stream));
+    std::lock_guard<std::mutex> lk(prof.mu);
     prof.events.emplace_back(e0, e1);
     double f = 2.0 * g.m * (double)g.n * g.k * g.batch;
     if (g.flags) {  // multiply-adds of the tiles actually computed
@@ -442,7 +443,7 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
       f *= g.batch;
     }
     prof.launch_flops.push_back(f);
-    prof.shapes.push_back({g.m, g.n, g.k, g.batch, g.flags, splits});
+    prof.shapes.push_back({g.m, g.n, g.k, g.batch, g.flags, splits, BM});
     prof.flops += f;
   }
   return kOk;

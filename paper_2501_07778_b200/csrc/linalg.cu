@@ -179,13 +179,13 @@ size_t panel_smem_bytes(int rpc, int pnb) {
 
 template <int PNB>
 int launch_panel_t(cudaStream_t s, const PanelArgs& pa0, int maxrows) {
-  static bool configured = false;
-  if (!configured) {
+  static DeviceFlag configured;
+  if (!configured.test()) {
     QTT_CUDA(cudaFuncSetAttribute(panel_qr_kernel<PNB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)panel_smem_bytes(maxrows, PNB)));
     QTT_CUDA(cudaFuncSetAttribute(panel_qr_kernel<PNB>,
                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured = true;
+    configured.set();
   }
   PanelArgs pa = pa0;
   // spread tall panels over up to 16 CTAs (>= 256 rows each) so the
@@ -697,13 +697,13 @@ __global__ void __launch_bounds__(MAXT) jacobi_ring_kernel(int p, int k, double*
 template <int E, int MAXT>
 int launch_ring_t(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw,
                   double tol, int cs, int ppc, size_t smem, const double* fd, double fs) {
-  static bool configured = false;
-  if (!configured) {
+  static DeviceFlag configured;
+  if (!configured.test()) {
     QTT_CUDA(cudaFuncSetAttribute(jacobi_ring_kernel<E, MAXT>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
     QTT_CUDA(cudaFuncSetAttribute(jacobi_ring_kernel<E, MAXT>,
                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured = true;
+    configured.set();
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs, 1, 1);
@@ -1071,13 +1071,13 @@ __global__ void __launch_bounds__(512) jacobi_pring_kernel(int p, int k, double*
 template <int EH>
 int launch_pring_t(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W, int64_t ldw,
                    double tol, int cs, int ppc, size_t smem, const double* fd, double fs) {
-  static bool configured = false;
-  if (!configured) {
+  static DeviceFlag configured;
+  if (!configured.test()) {
     QTT_CUDA(cudaFuncSetAttribute(jacobi_pring_kernel<EH>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
     QTT_CUDA(cudaFuncSetAttribute(jacobi_pring_kernel<EH>,
                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured = true;
+    configured.set();
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs, 1, 1);
@@ -1120,11 +1120,11 @@ int jacobi_gring(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W
   int cs = (int)ceil_div(np, 32);
   const int ppc = (int)ceil_div(np, cs);
   cs = (int)ceil_div(np, ppc);
-  static bool configured = false;
-  if (!configured) {
+  static DeviceFlag configured;
+  if (!configured.test()) {
     QTT_CUDA(cudaFuncSetAttribute(jacobi_gring_kernel,
                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured = true;
+    configured.set();
   }
   double* slots;
   QTT_CUDA(cudaMallocAsync(&slots, sizeof(double) * 4 * (size_t)np * ((size_t)p + k), s));
@@ -1486,13 +1486,13 @@ int small_qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double*
              double* R, int64_t ldr) {
   const size_t smem = sizeof(double) * (size_t)m * n;
   static const int dbg = getenv("QTT_SQR_DEBUG") ? 1 : 0;
-  static bool configured = false;
-  if (!configured) {
+  static DeviceFlag configured;
+  if (!configured.test()) {
     QTT_CUDA(cudaFuncSetAttribute(small_qr_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   SQ_MAXM * SQ_MAXN * 8));
     QTT_CUDA(cudaFuncSetAttribute(small_qr_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   SQ_MAXM * SQ_MAXN * 8));
-    configured = true;
+    configured.set();
   }
   if (m <= 128)
     small_qr_kernel<4><<<1, SQ_THREADS, smem, s>>>(m, n, A, lda, Q, ldq, R, ldr, dbg);
@@ -1659,11 +1659,11 @@ static int jacobi_impl(cudaStream_t s, int p, int k, double* X, int64_t ldx, dou
   }
   const size_t smem = sizeof(double) * ((size_t)p * k + (size_t)k * k);
   if (smem <= 200 * 1024) {
-    static bool configured = false;
-    if (!configured) {
+    static DeviceFlag configured;
+    if (!configured.test()) {
       QTT_CUDA(cudaFuncSetAttribute(jacobi_smem_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      configured = true;
+      configured.set();
     }
     const int threads = std::min(JTHREADS, std::max(32, ((k + 1) / 2) * 32));
     jacobi_smem_kernel<<<1, threads, smem, s>>>(p, k, X, ldx, W, ldw, tol, fd, fs);
@@ -1722,11 +1722,11 @@ int sort_chop(cudaStream_t s, int p, int k, const double* X, int64_t ldx, double
               int* perm, const double* delta_dev, double delta_scale, int rmax, int floor_rule,
               int* rank_dev) {
   if (k <= 0 || k > SORT_MAX) return kUnsupported;
-  static bool configured = false;
-  if (!configured) {
+  static DeviceFlag configured;
+  if (!configured.test()) {
     QTT_CUDA(cudaFuncSetAttribute(sort_chop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(2 * SORT_MAX * sizeof(double))));
-    configured = true;
+    configured.set();
   }
   sort_chop_kernel<<<1, 1024, 2 * k * sizeof(double), s>>>(p, k, X, ldx, sigma, perm, delta_dev, delta_scale, rmax,
                                       floor_rule, rank_dev);
@@ -1751,12 +1751,12 @@ int tri_inverse(cudaStream_t s, int k, const double* R, int64_t ldr, double* X) 
   const int64_t kk = k;
   QTT_CUDA(cudaMallocAsync(&T, sizeof(double) * kk * kk, s));
   QTT_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * kk * kk, s));
-  static bool configured = false;
+  static DeviceFlag configured;
   const int tri_smem = (int)((kBlk * (kBlk + 1) + 256 + kBlk) * sizeof(double));
-  if (!configured) {
+  if (!configured.test()) {
     QTT_CUDA(cudaFuncSetAttribute(trinv_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   tri_smem));
-    configured = true;
+    configured.set();
   }
   trinv_diag_kernel<<<(int)ceil_div(k, TRB), 256, tri_smem, s>>>(k, R, ldr, X, kk);
   QTT_CHECK_LAUNCH();

@@ -80,10 +80,10 @@ __global__ void axpy_kernel(int n, const double* __restrict__ d, double* __restr
 int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const double* b, double* x,
                 int* fallback) {
   if (N <= 0) return kInvalid;
-  static bool configured = false;
-  if (!configured) {
+  static DeviceFlag configured;
+  if (!configured.test()) {
     QTT_CUDA(cudaFuncSetAttribute(lu_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLuSmem));
-    configured = true;
+    configured.set();
   }
   const int64_t ld = N;
   const int nblk = (int)ceil_div(N, LB);

@@ -384,11 +384,11 @@ int tsqr_r(cudaStream_t s, int64_t rows, int m, const double* src, double* R) {
   int br = (int)std::min<int64_t>(4096, std::max<int64_t>(2 * m, 8192 / m));
   br = (br + 31) / 32 * 32;
   const size_t smem = sizeof(double) * (size_t)br * m;
-  static bool configured = false;
-  if (!configured) {
+  static DeviceFlag configured;
+  if (!configured.test()) {
     QTT_CUDA(cudaFuncSetAttribute(tsqr_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   100 * 1024));
-    configured = true;
+    configured.set();
   }
   const double* cur = src;
   int64_t cur_rows = rows;

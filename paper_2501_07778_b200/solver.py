@@ -86,7 +86,9 @@ class SolverConfig:
     # local tolerance is relaxed to local_rtol_factor * (latest known global
     # residual) while that exceeds the reference's 0.02 * epsilon, i.e.
     # inexact local solves in the early sweeps (no accuracy is lost at
-    # convergence: the bound tightens with the residual).
+    # convergence: the bound tightens with the residual).  Sweep s uses the
+    # residual of sweep s-2 on every path (the residual of sweep s-1 may
+    # still be in flight on the side stream when sweep s starts).
     local_rtol_factor: float = 0.0
 
     def __post_init__(self):
@@ -581,8 +583,12 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig, x0: TTVector | None = Non
 
     for sweep in range(cfg.max_sweeps):
         rtol_local = max(0.02 * cfg.epsilon * adapt, 1e-13)  # solver.py:296
-        if residual_rule and cfg.local_rtol_factor > 0.0 and residual_history:
-            rtol_local = max(rtol_local, min(cfg.local_rtol_factor * residual_history[-1], 1e-4))
+        if residual_rule and cfg.local_rtol_factor > 0.0 and sweep >= 2:
+            # residual of sweep s-2: on the speculative path that is the
+            # latest one known when sweep s starts (s-1's is still being
+            # evaluated), and the sequential path uses the same lag, so both
+            # paths follow the same iterates
+            rtol_local = max(rtol_local, min(cfg.local_rtol_factor * residual_history[sweep - 2], 1e-4))
         # ---------------- forward: solve + enrich ----------------
         for k in range(d):
             if poll():

@@ -29,12 +29,39 @@ def dense_of(t):
     return _T().tt_contract(t)
 
 
-def test_gemm_all_transposes():
+def _profiled(fn):
+    """Run fn with GEMM profiling on; return the dispatch record of its last launch."""
+    from paper_2501_07778_b200 import _lib
+
+    _lib.gemm_profile_start()
+    try:
+        fn()
+        torch.cuda.synchronize()
+        return _lib.gemm_profile_shapes(1)[0]
+    finally:
+        _lib.gemm_profile_stop()
+
+
+def _check_dispatch(rec, path):
+    """path: 'tiny' (32x32 tiles), 'tile64' (64x64, no split) or 'split' (64x64, split-K)."""
+    if path == "tiny":
+        assert rec["bm"] == 32 and rec["splits"] == 1, rec
+    elif path == "tile64":
+        assert rec["bm"] == 64 and rec["splits"] == 1, rec
+    else:
+        assert rec["bm"] == 64 and rec["splits"] > 1, rec
+
+
+@pytest.mark.parametrize("m,n,k,path", [(70, 45, 33, "tiny"), (1000, 700, 96, "tile64"),
+                                        (200, 150, 1100, "split")])
+def test_gemm_all_transposes(m, n, k, path):
+    """All four transpose variants of each kernel configuration (the dispatch
+    is asserted from the profiler record, so threshold changes cannot
+    silently drop coverage)."""
     T = _T()
-    rng = np.random.default_rng(0)
+    rng = np.random.default_rng(m + n + k)
     for ta in (0, 1):
         for tb in (0, 1):
-            m, n, k = 70, 45, 33
             a = rng.standard_normal((k, m) if ta else (m, k))
             b = rng.standard_normal((n, k) if tb else (k, n))
             c0 = rng.standard_normal((m, n))
@@ -42,25 +69,30 @@ def test_gemm_all_transposes():
             A = torch.tensor(np.asfortranarray(a).ravel(order="F"), device="cuda")
             B = torch.tensor(np.asfortranarray(b).ravel(order="F"), device="cuda")
             C = torch.tensor(c0.ravel(order="F"), device="cuda")
-            T._gemm(ta, tb, m, n, k, 0.5, A, a.shape[0], B, b.shape[0], 2.0, C, m)
+            rec = _profiled(lambda: T._gemm(ta, tb, m, n, k, 0.5, A, a.shape[0], B, b.shape[0], 2.0, C, m))
+            _check_dispatch(rec, path)
             want = 0.5 * (a.T if ta else a) @ (b.T if tb else b) + 2.0 * c0
             got = C.cpu().numpy().reshape((n, m)).T
-            assert np.abs(got - want).max() < 1e-12 * np.abs(want).max()
+            assert np.abs(got - want).max() < 1e-12 * np.sqrt(k) * np.abs(want).max()
 
 
 @pytest.mark.parametrize(
-    "m,n,k,ta,flags",
+    "m,n,k,ta,flags,path",
     [
-        (64, 64, 64, 0, 2 | 4),          # 32x32 tiles, both operands upper triangular
-        (512, 512, 512, 0, 4),           # split-K, B upper (tri-inverse level)
-        (512, 512, 512, 0, 2),           # split-K, A upper
-        (1024, 1024, 4096, 1, 1),        # upper-C Gram, split over the computing tiles only
-        (2048, 2048, 2048, 0, 2 | 4),    # longest-reduction-first tile order
-        (1000, 1000, 1000, 0, 1 | 8 | 4),  # upper C, A lower, B upper, ragged tiles
-        (700, 300, 700, 0, 16),          # B lower triangular
+        (64, 64, 64, 0, 2 | 4, "tiny"),          # 32x32 tiles, both operands upper triangular
+        (512, 512, 512, 0, 4, "tiny"),           # B upper on the 32x32 tiles
+        (512, 512, 2048, 0, 4, "split"),         # split-K, B upper (per-chunk K clipping)
+        (512, 512, 2048, 0, 2, "split"),         # split-K, A upper
+        (512, 512, 2048, 0, 8, "split"),         # split-K, A lower
+        (700, 300, 1400, 0, 16, "split"),        # split-K, B lower
+        (1024, 1024, 4096, 1, 1, "split"),       # upper-C Gram, split over the computing tiles only
+        (2048, 2048, 2048, 0, 2 | 4, "tile64"),  # longest-reduction-first tile order
+        (1000, 1000, 1000, 0, 1 | 8 | 4, "split"),  # upper C, A lower, B upper, ragged tiles
+        (700, 300, 700, 0, 16, "tiny"),          # B lower triangular
+        (1200, 1100, 300, 0, 2 | 16, "tile64"),  # A upper, B lower, 64x64 tiles without split
     ],
 )
-def test_gemm_structured(m, n, k, ta, flags):
+def test_gemm_structured(m, n, k, ta, flags, path):
     """Structure-flagged DMMA GEMM (upper-C tiles, triangular operand
     clipping, split-K, tile order) against the dense float64 product."""
     rng = np.random.default_rng(m + 7 * n + k + flags)
@@ -83,10 +115,12 @@ def test_gemm_structured(m, n, k, ta, flags):
     from paper_2501_07778_b200 import _lib
     import ctypes
 
-    _lib.call("qtt_gemm_structured", ctypes.c_int32(ta), ctypes.c_int32(0), ctypes.c_int64(m),
-              ctypes.c_int64(n), ctypes.c_int64(k), ctypes.c_double(-0.5), _lib.ptr(A),
-              ctypes.c_int64(a.shape[0]), _lib.ptr(B), ctypes.c_int64(k), ctypes.c_double(1.5),
-              _lib.ptr(C), ctypes.c_int64(m), ctypes.c_int32(flags), _lib.stream_handle())
+    rec = _profiled(lambda: _lib.call(
+        "qtt_gemm_structured", ctypes.c_int32(ta), ctypes.c_int32(0), ctypes.c_int64(m),
+        ctypes.c_int64(n), ctypes.c_int64(k), ctypes.c_double(-0.5), _lib.ptr(A),
+        ctypes.c_int64(a.shape[0]), _lib.ptr(B), ctypes.c_int64(k), ctypes.c_double(1.5),
+        _lib.ptr(C), ctypes.c_int64(m), ctypes.c_int32(flags), _lib.stream_handle()))
+    _check_dispatch(rec, path)
     want = -0.5 * opa @ b + 1.5 * c0
     got = C.cpu().numpy().reshape((n, m)).T
     if flags & 1:  # only the upper triangle (incl. diagonal) is specified
