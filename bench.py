@@ -94,6 +94,15 @@ def matvec_cost(rA, rx, d=D):
     return flops, byts
 
 
+WORKLOAD = ("config2: TT matvec (d=24, rA in {4,8,16}, rx in {16,64,128}) + tt_round eps=1e-10, "
+            "all 9 pairs per step")
+
+
+def config_dict(flops):
+    """The ``config`` object both arms print (identical keys and values)."""
+    return {"workload": WORKLOAD, "gflop_per_step": round(flops / 1e9, 3)}
+
+
 def step_flops(pairs):
     tot = 0.0
     for rA, rx in pairs:
@@ -354,9 +363,8 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded, SURVEY.md §8(d))",
-            "config": {
-                "workload": "config2: TT matvec (d=24, rA in {4,8,16}, rx in {16,64,128}) + tt_round eps=1e-10, all 9 pairs per step",
-                "gflop_per_step": round(flops / 1e9, 3),
+            "config": config_dict(flops),
+            "config_notes": {
                 "pairs": "serial" if args.serial else "concurrent (one stream per pair)",
                 "l2": "flushed between steps (256 MiB write); y cores up to 1.48 GB exceed L2",
                 "parallelism": f"replicas x{world}",
@@ -380,10 +388,16 @@ def run_ours(args):
                 "gemm_launches_per_step": int(glaunch),
                 "gemm_share_of_step": round(gms / serial_ms, 4),
                 "step_nominal_tflops_frac": round(value / 1e3 / fp64_peak, 4),
+                "executed_gemm_gflop_per_step": round(gflop / 1e9, 3),
+                "nominal_gflop_per_step": round(flops / 1e9, 3),
+                "step_executed_tflops": round(gflop / (serial_ms * 1e-3) / 1e12, 3),
+                "step_executed_frac": round(gflop / (serial_ms * 1e-3) / 1e12 / fp64_peak, 4),
                 "note": "frac = executed-flop rate of the DMMA GEMMs (per-launch events, serial pass); "
-                        "step_nominal_tflops_frac = SURVEY 8(d) nominal flops of the whole step / time / "
-                        "peak, which exceeds 1 because the no-truncation certificate skips SVDs the "
-                        "nominal (reference) count includes",
+                        "step_executed_frac = GEMM flops actually executed in one serial step / serial "
+                        "step time / peak (QR panels, Jacobi and Cholesky work not counted); "
+                        "step_nominal_tflops_frac = SURVEY 8(d) nominal (reference-shape) flops / "
+                        "concurrent step time / peak, which exceeds 1 because the no-truncation "
+                        "certificate skips SVDs the nominal count includes",
                 "serial_step_ms": round(serial_ms, 3),
             },
             "matvec_roofline": {
@@ -401,7 +415,7 @@ def run_ours(args):
             },
             "clocks": clk,
             "solve_wall_s": None if not extras else {
-                k: extras["solves"][k]["total_s"] for k in ("config4_d10", "config4_constE_d10", "config1_d5")
+                k: extras["solves"][k]["total_s"] for k in ("config4_d10", "config5_d10", "config4_constE_d10", "config1_d5")
                 if k in extras["solves"]},
             "cpu_baseline": cpu,
             "extras": extras,
@@ -425,22 +439,76 @@ def _dev_ms(torch, fn):
     return out, e0.elapsed_time(e1)
 
 
-def run_extras(torch, T, cpu_baseline=True) -> dict:
-    """Configs 3, 1 and the 2^10 x 2^10 solves: config 4 as specified
-    (variable E, upgraded AMEn: local-residual truncation, enrichment 24,
-    local tolerance relaxed to 1e-3 x the last residual in early sweeps,
-    device GMRES local solves) and its constant-E variant on the
-    reference's own solver path (dense local solves), device-synchronised
-    wall time."""
+UPGRADED = dict(local_solver="auto", truncation="residual", enrichment_rank=24, local_rtol_factor=1e-3)
+# config 5: same upgraded solver, tighter truncation factor, stop at the FP64
+# residual floor (stall rule): ||K|| ||u|| / ||f|| ~ 1e8 at d=10
+CONFIG5 = dict(UPGRADED, trunc_factor=0.05, stall_sweeps=4, max_sweeps=30)
+
+
+def _conforming_error(T, u, idx, d):
+    """||u - u_conf|| / ||u_conf|| against the committed conforming ground
+    truth (tests/golden/conforming_c*_d*.npz), or None if absent."""
+    path = os.path.join(ROOT, "tests", "golden", f"conforming_c{idx}_d{d}.npz")
+    if not os.path.exists(path):
+        return None
+    c = np.load(path)
+    uc = T.TTVector([c[f"cores_{k}"] for k in range(len(c["ranks"]) - 1)])
+    return float(T.tt_norm(T.tt_sub(u, uc)) / T.tt_norm(uc))
+
+
+def _timed_build_solve(torch, T, S, build_system, idx, d, kw):
     import time as _t
+
+    tm = {}
+    torch.cuda.synchronize()
+    t0 = _t.perf_counter()
+    gsys, eps = build_system(idx, d, tm)
+    t1 = _t.perf_counter()
+    res = S.solve(gsys.K, gsys.f, S.SolverConfig(epsilon=eps, seed=0, **kw))
+    torch.cuda.synchronize()
+    t2 = _t.perf_counter()
+    out = {
+        "solver": kw,
+        "build_s": round(t1 - t0, 3), **{k: round(v, 3) for k, v in tm.items()},
+        "solve_s": round(t2 - t1, 3), "total_s": round(t2 - t0, 3), "sweeps": res.sweeps,
+        "residual": res.residual, "converged": res.converged, "max_rank": max(res.u.ranks),
+        "K_max_rank": max(gsys.K.ranks),
+    }
+    return out, gsys, res
+
+
+def run_extras(torch, T, cpu_baseline=True) -> dict:
+    """Configs 3, 1, 4 and 5 next to the config-2 line, device-synchronised:
+
+    * config 3: rounding (both eps) and the 2^26 TT-SVD, with the oracle port
+      timed on this host in the same run;
+    * solves: config 1 (reference solver path), config 4 as specified
+      (variable E, upgraded AMEn -- the reference cannot solve it,
+      profiles/r02_ref_solve_c4_d6.log), config-4 geometry with constant E on
+      the reference path, config 5 (L-shape) with the stall rule, each with
+      the forward error against the conforming ground truth when the fixture
+      exists;
+    * same-run CPU solve baseline: the oracle AMEn port (local_solver
+      "direct", all host threads) on config 1 and on the config-4 geometry
+      with constant E at d=6, next to the device solve of the same systems;
+    * a truncating rounding: config 4's Dirichlet round(D K D) (rank 1,712
+      -> 117), with its nominal flops (SURVEY §8(d) formula).
+    """
+    import time as _t
+
+    from paper_2501_07778_b200 import solver as S
+    from paper_2501_07778_b200.configs import build_system
 
     out = {}
     # ---- config 3: rounding of a 16-term rank-8 sum (d=26) and TT-SVD of 2^26
     rng = np.random.default_rng(3000)
     acc = None
+    host_terms = []
     for _ in range(16):
         rk = [1] + [8] * 25 + [1]
-        t = T.TTVector([rng.standard_normal((rk[k], 2, rk[k + 1])) / np.sqrt(8) for k in range(26)])
+        cores = [rng.standard_normal((rk[k], 2, rk[k + 1])) / np.sqrt(8) for k in range(26)]
+        host_terms.append(cores)
+        t = T.TTVector(cores)
         acc = t if acc is None else T.tt_add(acc, t)
     c3 = {}
     for eps in (1e-6, 1e-10):
@@ -459,52 +527,102 @@ def run_extras(torch, T, cpu_baseline=True) -> dict:
     c3["ttsvd_2^26_ms"] = round(ms, 3)
     c3["ttsvd_ranks_equal_reference"] = tv.ranks == SURVEY_C3_TTSVD_RANKS
     c3["ttsvd_hbm_roofline_ms"] = round(4.17e9 / 6543.4e9 * 1e3, 3)
-    c3["reference_cpu_s"] = {"round_each_eps": 0.175, "ttsvd": 10.59, "source": "SURVEY Appendix B, 8-core Xeon"}
-    out["config3"] = c3
-    # ---- solves
-    from paper_2501_07778_b200 import solver as S
-    from paper_2501_07778_b200.configs import build_system
-
-    solves = {}
-    upgraded = dict(local_solver="auto", truncation="residual", enrichment_rank=24, local_rtol_factor=1e-3)
-    for idx, d, kw in ((1, 5, dict(local_solver="direct")), (4, 10, upgraded),
-                       (40, 10, dict(local_solver="direct"))):
-        tm = {}
-        torch.cuda.synchronize()
-        t0 = _t.perf_counter()
-        gsys, eps = build_system(idx, d, tm)
-        t1 = _t.perf_counter()
-        res = S.solve(gsys.K, gsys.f, S.SolverConfig(epsilon=eps, seed=0, **kw))
-        torch.cuda.synchronize()
-        t2 = _t.perf_counter()
-        solves[f"config{idx if idx != 40 else '4_constE'}_d{d}"] = {
-            "solver": kw,
-            "build_s": round(t1 - t0, 3), **{k: round(v, 3) for k, v in tm.items()},
-            "solve_s": round(t2 - t1, 3), "total_s": round(t2 - t0, 3), "sweeps": res.sweeps,
-            "residual": res.residual, "converged": res.converged, "max_rank": max(res.u.ranks),
-            "K_max_rank": max(gsys.K.ranks),
-        }
-    solves["reference_cpu_s"] = {"config1_d5_solve": 1.21, "config4_constE_d10_solve": 658.9,
-                                 "config4_constE_d10_assembly": 11.05,
-                                 "config4_d10_assembly": 43.0, "config4_d10_couple_dirichlet": 18.0,
-                                 "config4_d10_solve": None,
-                                 "note": "the reference solver does not converge on config 4 (variable E): "
-                                         "default GMRES local solves diverge, direct local solves grow "
-                                         "ranks toward max_rank (DESIGN.md 8)",
-                                 "source": "SURVEY Appendix B / BASELINE.md, 8-core Xeon"}
     if cpu_baseline:
-        # reference algorithm (oracle restatement) on this host: config 1 solve
+        from oracle import tt as O
+
+        host_acc = host_terms[0]
+        for t in host_terms[1:]:
+            host_acc = O.add(host_acc, t)
+        t0 = _t.perf_counter()
+        O.round_tt(host_acc, 1e-10)
+        c3["cpu_round_eps1e-10_s"] = round(_t.perf_counter() - t0, 3)
+        vh = v.cpu().numpy()
+        t0 = _t.perf_counter()
+        O.decompose_vector(vh, 1e-8)
+        c3["cpu_ttsvd_s"] = round(_t.perf_counter() - t0, 3)
+        c3["cpu_cores"] = os.cpu_count()
+        c3["cpu_kind"] = "port (oracle/tt.py, numpy/OpenBLAS all threads)"
+    del v, X, Y, xs
+    out["config3"] = c3
+
+    # ---- solves
+    solves = {}
+    runs = (("config1_d5", 1, 5, dict(local_solver="direct")),
+            ("config4_d10", 4, 10, UPGRADED),
+            ("config4_constE_d10", 40, 10, dict(local_solver="direct")),
+            ("config5_d10", 5, 10, CONFIG5))
+    saved_bits = S._DENSE_RESIDUAL_BITS
+    for name, idx, d, kw in runs:
+        if idx == 5:
+            S._DENSE_RESIDUAL_BITS = 23  # 2^23 dense residual
+        try:
+            rec, gsys, res = _timed_build_solve(torch, T, S, build_system, idx, d, kw)
+        finally:
+            S._DENSE_RESIDUAL_BITS = saved_bits
+        rec["conforming_rel_error"] = _conforming_error(T, res.u, idx, d)
+        solves[name] = rec
+        del gsys, res
+        _release(torch)
+    solves["reference_cpu_s_survey"] = {
+        "config1_d5_solve": 1.21, "config4_constE_d10_solve": 658.9, "config4_constE_d10_assembly": 11.05,
+        "config4_d10_assembly": 43.0, "config4_d10_couple_dirichlet": 18.0,
+        "note": "SURVEY Appendix B (8-core Xeon); the reference solver does not converge on config 4 "
+                "as specified (variable E), profiles/r02_ref_solve_c4_d6.log"}
+    if cpu_baseline:
         from oracle import amen
 
-        gsys, eps = build_system(1, 5)
-        K = [c.cpu().numpy() for c in gsys.K.cores]
-        f = [c.cpu().numpy() for c in gsys.f.cores]
-        t0 = _t.perf_counter()
-        r = amen.solve(K, f, eps=eps, seed=0)
-        solves["cpu_oracle_config1_d5_solve_s"] = round(_t.perf_counter() - t0, 3)
-        solves["cpu_oracle_config1_sweeps"] = r["sweeps"]
+        same = {}
+        for name, idx, d in (("config1_d5", 1, 5), ("config4_constE_d6", 40, 6)):
+            gsys, eps = build_system(idx, d)
+            K = [c.cpu().numpy() for c in gsys.K.cores]
+            f = [c.cpu().numpy() for c in gsys.f.cores]
+            t0 = _t.perf_counter()
+            r = amen.solve(K, f, eps=eps, seed=0)
+            cpu_s = _t.perf_counter() - t0
+            torch.cuda.synchronize()
+            t0 = _t.perf_counter()
+            g = S.solve(gsys.K, gsys.f, S.SolverConfig(epsilon=eps, seed=0, local_solver="direct"))
+            torch.cuda.synchronize()
+            gpu_s = _t.perf_counter() - t0
+            same[name] = {"cpu_solve_s": round(cpu_s, 3), "cpu_sweeps": r["sweeps"],
+                          "cpu_residual": r["residual"], "gpu_solve_s": round(gpu_s, 3),
+                          "gpu_sweeps": g.sweeps, "gpu_residual": g.residual,
+                          "speedup": round(cpu_s / gpu_s, 1)}
+        same["cores"] = os.cpu_count()
+        same["kind"] = "port (oracle/amen.py: reference AMEn restated, local_solver='direct', OpenBLAS all threads)"
+        solves["same_run_cpu_solve"] = same
     out["solves"] = solves
+
+    # ---- a truncating rounding: config 4's Dirichlet round(D K D)
+    from paper_2501_07778_b200.assembly import assemble_subdomain
+    from paper_2501_07778_b200.configs import config
+    from paper_2501_07778_b200.coupling import concat_blocks
+    from paper_2501_07778_b200.topology import DomainTopology
+
+    meshes, mat, body, eps = config(4, 10)
+    systems = [assemble_subdomain(m, mat, "zorder", eps, body_force=body) for m in meshes]
+    g = concat_blocks(systems, DomainTopology.from_subdomains(meshes), ordering="zorder", epsilon=eps)
+    dmask = T.tt_diag(g.mask)
+    dkd = T.tt_matmat(dmask, T.tt_matmat(g.K, dmask))
+    T.tt_round(dkd, eps)
+    kr, ms = _dev_ms(torch, lambda: T.tt_round(dkd, eps))
+    nominal = round_flops(list(dkd.ranks), list(kr.ranks), n=4)
+    out["dirichlet_round"] = {
+        "ms": round(ms, 3), "pre_round_max_rank": max(dkd.ranks), "out_max_rank": max(kr.ranks),
+        "nominal_gflop": round(nominal / 1e9, 2),
+        "nominal_tflops": round(nominal / (ms * 1e-3) / 1e12, 3),
+        "note": "truncating rounding (one-sided Jacobi path); nominal = SURVEY 8(d) QR + R-SVD count over the "
+                "shapes tt_round visits"}
     return out
+
+
+def _release(torch):
+    try:
+        from paper_2501_07778_b200 import _lib
+
+        _lib.release_cached()
+    except Exception:
+        torch.cuda.empty_cache()
 
 
 def load_peaks() -> dict:
@@ -591,10 +709,7 @@ def run_reference(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded, SURVEY.md §8(d))",
-        "config": {
-            "workload": "config2: TT matvec (d=24, rA in {4,8,16}, rx in {16,64,128}) + tt_round eps=1e-10, all 9 pairs per step",
-            "gflop_per_step": round(flops / 1e9, 3),
-        },
+        "config": config_dict(flops),
         "cpu_baseline": {
             "value": round(value, 3),
             "unit": "GFLOP/s",

@@ -206,7 +206,7 @@ def main(idx: int, d: int):
     free = ~system.constrained
     kff = system.K[free][:, free].tocsr()
     ff = system.f[free]
-    if topo.q == 1:
+    if topo.q == 1 or free.sum() <= 2_500_000:
         uf = spla.splu(kff.tocsc(), permc_spec="MMD_AT_PLUS_A").solve(ff)
     else:
         uf = schur_solve(system, free, kff, ff)
