@@ -574,8 +574,8 @@ def run_extras(torch, T, cpu_baseline=True) -> dict:
         same = {}
         for name, idx, d in (("config1_d5", 1, 5), ("config4_constE_d6", 40, 6)):
             gsys, eps = build_system(idx, d)
-            K = [c.cpu().numpy() for c in gsys.K.cores]
-            f = [c.cpu().numpy() for c in gsys.f.cores]
+            K = list(gsys.K.cores)  # host numpy copies
+            f = list(gsys.f.cores)
             t0 = _t.perf_counter()
             r = amen.solve(K, f, eps=eps, seed=0)
             cpu_s = _t.perf_counter() - t0

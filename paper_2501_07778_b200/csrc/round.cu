@@ -416,6 +416,23 @@ int tsqr_r(cudaStream_t s, int64_t rows, int m, const double* src, double* R) {
 
 }  // namespace
 
+struct TtsvdFast {
+  bool done = false, zero = false;
+  int l = 0, r = 1;
+  std::vector<int> ranks;
+  double* stage = nullptr;
+  double* carry = nullptr;
+  double* owned[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t s = nullptr;
+  void release() {
+    for (auto& p : owned)
+      if (p) cudaFreeAsync(p, s), p = nullptr;
+  }
+};
+int ttsvd_fast(cudaStream_t s, const double* dense, int d, const int64_t* sizes, double eps,
+               TtsvdFast& res);                                                   // ttsvd.cu
+int ttsvd_pack(cudaStream_t s, int d, const double* stage, const qtt_layout* out, double* out_data);
+
 int decompose(const double* dense, int d, const int64_t* sizes, double eps, qtt_layout* out,
               double* out_data, int64_t capacity, cudaStream_t s) {
   if (d < 1 || d > QTT_MAX_CORES || eps < 0) return kInvalid;
@@ -429,6 +446,32 @@ int decompose(const double* dense, int d, const int64_t* sizes, double eps, qtt_
   for (int l = 0; l < d; ++l) {
     out->rows[l] = sizes[l];
     out->cols[l] = 1;
+  }
+  // device-resident supersteps (ttsvd.cu) while r_l n_l <= 64; the per-step
+  // path below finishes when a rank outgrows them
+  TtsvdFast fast;
+  int l_start = 0;
+  {
+    const int st = ttsvd_fast(s, dense, d, sizes, eps, fast);
+    if (st != kOk && st != kUnsupported) {
+      fast.release();
+      return st;
+    }
+    if (st == kOk && (fast.done || fast.zero)) {
+      for (int l = 0; l <= d; ++l) out->ranks[l] = fast.zero ? 1 : fast.ranks[l];
+      out->ranks[0] = out->ranks[d] = 1;
+      pack_offsets(out);
+      if (packed_size(out) > capacity) {
+        fast.release();
+        return kWorkspace;
+      }
+      const int pst = ttsvd_pack(s, d, fast.stage, out, out_data);
+      fast.release();
+      QTT_TRY(pst);
+      QTT_CUDA(cudaStreamSynchronize(s));
+      return kOk;
+    }
+    if (st == kOk) l_start = fast.l;  // handoff
   }
   DevBuf sc;
   QTT_TRY(sc.alloc(s, 16));
@@ -456,8 +499,25 @@ int decompose(const double* dense, int d, const int64_t* sizes, double eps, qtt_
   const double* cur = dense;
   int64_t rest = total;
   int rp = 1;
+  if (l_start > 0) {  // cores 0..l_start-1 and the carry come from the supersteps
+    for (int l = 0; l < l_start; ++l) {
+      rk[l + 1] = fast.ranks[l + 1];
+      const int64_t len = rk[l] * sizes[l] * rk[l + 1];
+      QTT_TRY(cores[l].alloc(s, len));
+      QTT_CUDA(cudaMemcpyAsync(cores[l].p, fast.stage + (int64_t)l * 4096, sizeof(double) * len,
+                               cudaMemcpyDeviceToDevice, s));
+    }
+    rp = fast.r;
+    rest = 1;
+    for (int l = l_start; l < d; ++l) rest *= sizes[l];
+    DevBuf& hold = carry[(l_start & 1) ^ 1];  // the slot the first per-step iteration does not reuse
+    QTT_TRY(hold.alloc(s, (int64_t)rp * rest));
+    QTT_CUDA(cudaMemcpyAsync(hold.p, fast.carry, sizeof(double) * rp * rest, cudaMemcpyDeviceToDevice, s));
+    cur = hold.p;
+  }
+  fast.release();
   DevBuf R, W, Xb, sig, permb, Ub, Qb, Zp;
-  for (int l = 0; l < d - 1; ++l) {
+  for (int l = l_start; l < d - 1; ++l) {
     const int n = (int)sizes[l];
     const int m = rp * n;
     const int64_t N = rest / n;

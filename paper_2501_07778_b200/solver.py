@@ -146,7 +146,7 @@ def _apply_tt_to_tt(K: TTMatrix, u: TTVector) -> torch.Tensor:
     ~ 2^(D/2) r_K r_u (r_K + r_u) per core plus 2^D r_K r_u, against
     ~ 2^D r_K^2 per core for the dense chain over a materialised u (about 5x
     fewer at the config-4 ranks).  Returns the flat (row-index) vector."""
-    Kc, uc = K.cores, u.cores
+    Kc, uc = K.device_cores, u.device_cores
     D = len(uc)
     m = D // 2
     dev = u.data.device
@@ -182,7 +182,7 @@ def residual(K: TTMatrix, u: TTVector, f: TTVector, rounding_eps=None) -> float:
     fn = tt_norm(f)
     if fn == 0.0:
         return 0.0
-    if len(u.cores) <= _DENSE_RESIDUAL_BITS:
+    if len(u.device_cores) <= _DENSE_RESIDUAL_BITS:
         fd = tt_contract_device(f)
         r = _apply_tt_to_tt(K, u) - fd
         return float(torch.linalg.vector_norm(r) / torch.linalg.vector_norm(fd))
@@ -497,7 +497,7 @@ def _init_cores(rng, sizes, rank, dev):
 def _operator_views(K: TTMatrix):
     """Per-core permuted copies of the operator cores used by the GEMMs."""
     views = []
-    for c in K.cores:
+    for c in K.device_cores:
         ra, n, m, rb = c.shape
         views.append({
             "ra": ra, "rb": rb, "n": n,
@@ -535,9 +535,9 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig, x0: TTVector | None = Non
     if x0 is not None:
         if x0.mode_sizes != sizes:
             raise ValueError("initial guess modes do not match the right-hand side")
-        x = _right_orthogonalize_all([c.contiguous().clone() for c in x0.cores])
+        x = _right_orthogonalize_all([c.contiguous().clone() for c in x0.device_cores])
     A = _operator_views(K)
-    F = [c.contiguous() for c in f.cores]
+    F = [c.contiguous() for c in f.device_cores]
 
     one3 = torch.ones((1, 1, 1), dtype=torch.float64, device=dev)
     one2 = torch.ones((1, 1), dtype=torch.float64, device=dev)

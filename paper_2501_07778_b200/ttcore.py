@@ -61,7 +61,7 @@ def _offsets(shapes) -> tuple:
 class _TT:
     """Common storage of TTVector / TTMatrix."""
 
-    __slots__ = ("data", "_shapes", "_offs")
+    __slots__ = ("data", "_shapes", "_offs", "_host")
     _order = 3
 
     def __init__(self, cores):
@@ -103,6 +103,7 @@ class _TT:
         self.data = data
         self._shapes = tuple(shapes)
         self._offs = offs
+        self._host = None
 
     @classmethod
     def _wrap(cls, data: torch.Tensor, shapes, offs=None):
@@ -110,14 +111,29 @@ class _TT:
         obj.data = data
         obj._shapes = tuple(tuple(int(x) for x in s) for s in shapes)
         obj._offs = tuple(offs) if offs is not None else _offsets(obj._shapes)[0]
+        obj._host = None
         return obj
 
     # -------------------------------------------------------------- views
     @property
-    def cores(self) -> tuple:
+    def device_cores(self) -> tuple:
+        """The cores as CUDA tensor views of the packed buffer (no copy)."""
         return tuple(
             self.data[o : o + int(np.prod(s))].view(s) for o, s in zip(self._offs, self._shapes)
         )
+
+    @property
+    def cores(self) -> tuple:
+        """The cores as read-only host numpy arrays, like the reference's
+        frozen cores (ttcore.py:49-52,61,71): one D2H copy on first access,
+        cached (the object is immutable).  Device code uses device_cores."""
+        host = getattr(self, "_host", None)
+        if host is None:
+            host = tuple(self.numpy_cores())
+            for a in host:
+                a.flags.writeable = False
+            self._host = host
+        return host
 
     def numpy_cores(self) -> list:
         """Host copies of the cores: one D2H copy of the packed buffer into
@@ -489,7 +505,7 @@ def tt_kron(A, B):
     """Kronecker product, B's cores first (ttcore.py:489-498)."""
     if isinstance(A, TTVector) != isinstance(B, TTVector):
         raise ValueError("cannot mix vectors and matrices")
-    return _concat(type(A), list(B.cores) + list(A.cores))
+    return _concat(type(A), list(B.device_cores) + list(A.device_cores))
 
 
 def _concat(kind, cores):
@@ -553,7 +569,7 @@ def tt_slice_mode(t, mode: int, index: int):
         raise ValueError("mode out of range")
     if t.d == 1:
         raise ValueError("cannot slice away the only mode")
-    cores = list(t.cores)
+    cores = list(t.device_cores)
     sl = cores[mode][:, index, :].contiguous()  # (r0, r1)
     del cores[mode]
     if mode == 0:

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_ttsvd.py tests/test_gpu_ttcore.py tests/test_gpu_scale.py -q -k "decompose or ttsvd or config3 or low_rank or smooth or handoff or graded or mode_size or zero" > gpurun_out/g7_tests.txt 2>&1
+echo "rc=$?" >> gpurun_out/g7_tests.txt
+python tools/ttsvd_profile.py > gpurun_out/g7_plain.txt 2>&1
+ncu --nvtx --nvtx-include "ttsvd/" --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/g7_ttsvd_launches.csv python tools/ttsvd_profile.py > gpurun_out/g7_ncu.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_fem.py tests/test_gpu_solver.py -q -x > gpurun_out/g7_tests2.txt 2>&1
+echo "rc=$?" >> gpurun_out/g7_tests2.txt

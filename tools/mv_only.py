@@ -10,4 +10,4 @@ for _ in range(int(sys.argv[2]) if len(sys.argv) > 2 else 3):
 torch.cuda.synchronize()
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 e0.record(); y = T.tt_matvec(TA, tx); e1.record(); torch.cuda.synchronize()
-print("matvec ms", e0.elapsed_time(e1), "GB/s", 8 * sum(c.numel() for c in y.cores) / e0.elapsed_time(e1) / 1e6)
+print("matvec ms", e0.elapsed_time(e1), "GB/s", 8 * sum(c.numel() for c in y.device_cores) / e0.elapsed_time(e1) / 1e6)
