@@ -47,6 +47,36 @@ int fetch(cudaStream_t s, const T* dev, T* host) {
   return kOk;
 }
 
+
+// QTT_ROUND_TRACE=1: synchronising per-phase timer (diagnostics only).
+struct PhaseTimer {
+  bool on;
+  cudaStream_t s;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  explicit PhaseTimer(cudaStream_t st) : on(getenv("QTT_ROUND_TRACE") != nullptr), s(st) {
+    if (on) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, s);
+    }
+  }
+  void lap(const char* what, int k, int a, int b, int c) {
+    if (!on) return;
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    fprintf(stderr, "[round] %-10s k=%2d %5d x %5d (%5d) %8.3f ms\n", what, k, a, b, c, ms);
+    cudaEventRecord(e0, s);
+  }
+  ~PhaseTimer() {
+    if (on) {
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+  }
+};
+
 // Right-to-left orthogonalisation of merged order-3 cores held in slots.
 // A core whose right unfolding is wide (n_k r_{k+1} < r_k) needs no QR: the
 // unfolding itself is the carry and the core becomes the identity, which is
