@@ -232,7 +232,69 @@ int chol_upper(cudaStream_t s, int n, double* G, int64_t ldg, double* rblk, int*
   return kOk;
 }
 
+__global__ void gram_trace_kernel(int n, const double* __restrict__ G, int64_t ldg, double* out) {
+  __shared__ double red[32];
+  double a = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) a += G[i + (int64_t)i * ldg];
+  a = warp_sum(a);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    *out = t;
+  }
+}
+
+// sc[0] = ||X||_F^2 (trace of G), sc[1] = ||R^{-1}||_F
+__global__ void gram_certificate_kernel(int p, int r, const double* sc, const int* bad,
+                                        const double* delta_dev, double delta_scale, int* ok,
+                                        int debug) {
+  const double eps = 2.220446049250313e-16;
+  const double x2 = sc[0], xn = sc[1];
+  const double delta = delta_dev ? (*delta_dev) * delta_scale : 0.0;
+  const double thr = 1.25 * fmax(delta, sqrt(fmax(x2, 0.0)) * (double)max(r, 2) * eps);
+  const double lower = 1.0 / (xn * xn) - 2.0 * (double)(p + r + 2) * eps * x2;
+  const bool good = !*bad && isfinite(xn) && isfinite(x2) && xn > 0.0 && lower > thr * thr;
+  *ok = good ? 1 : 0;
+  if (debug)
+    printf("[gram-cert] p=%d r=%d smin^2/|X|^2 >= %.3e thr^2/|X|^2=%.3e bad=%d good=%d\n", p, r,
+           lower / x2, thr * thr / x2, *bad, (int)good);
+}
+
 }  // namespace
+
+int gram_certificate(cudaStream_t s, int p, int r, const double* X, int64_t ldx,
+                     const double* delta_dev, double delta_scale, int* ok_dev) {
+  if (p < r || r <= 0) return kInvalid;
+  const int64_t nn = r;
+  double *G, *Ri, *rblk, *sc;
+  int* bad;
+  QTT_CUDA(cudaMallocAsync(&G, sizeof(double) * nn * nn, s));
+  QTT_CUDA(cudaMallocAsync(&Ri, sizeof(double) * nn * nn, s));
+  QTT_CUDA(cudaMallocAsync(&rblk, sizeof(double) * CB * CB * ceil_div(nn, CB), s));
+  QTT_CUDA(cudaMallocAsync(&sc, sizeof(double) * 4, s));
+  QTT_CUDA(cudaMallocAsync(&bad, sizeof(int), s));
+  QTT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  int status = kOk;
+  do {
+    if ((status = dgemm(s, 1, 0, r, r, p, 1.0, X, ldx, X, ldx, 0.0, G, nn, kGemmUpperC)) != kOk) break;
+    gram_trace_kernel<<<1, 256, 0, s>>>(r, G, nn, sc);
+    QTT_CHECK_LAUNCH();
+    if ((status = chol_upper(s, r, G, nn, rblk, bad)) != kOk) break;
+    if ((status = tri_inverse(s, r, G, nn, Ri)) != kOk) break;
+    if ((status = frob_norm(s, nn * nn, Ri, sc + 1)) != kOk) break;
+    static const int debug = getenv("QTT_CERT_DEBUG") ? 1 : 0;
+    gram_certificate_kernel<<<1, 1, 0, s>>>(p, r, sc, bad, delta_dev, delta_scale, ok_dev, debug);
+    QTT_CHECK_LAUNCH();
+  } while (false);
+  QTT_CUDA(cudaFreeAsync(G, s));
+  QTT_CUDA(cudaFreeAsync(Ri, s));
+  QTT_CUDA(cudaFreeAsync(rblk, s));
+  QTT_CUDA(cudaFreeAsync(sc, s));
+  QTT_CUDA(cudaFreeAsync(bad, s));
+  return status;
+}
 
 int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
             double* R, int64_t ldr, int* ok) {

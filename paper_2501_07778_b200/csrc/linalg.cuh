@@ -2,7 +2,38 @@
 #pragma once
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace qtt {
+// QTT_ROUND_TRACE=1: synchronising per-phase timer (diagnostics only).
+struct PhaseTimer {
+  bool on;
+  cudaStream_t s;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  explicit PhaseTimer(cudaStream_t st) : on(getenv("QTT_ROUND_TRACE") != nullptr), s(st) {
+    if (on) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, s);
+    }
+  }
+  void lap(const char* what, int k, int a, int b, int c) {
+    if (!on) return;
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    fprintf(stderr, "[round] %-10s k=%2d %5d x %5d (%5d) %8.3f ms\n", what, k, a, b, c, ms);
+    cudaEventRecord(e0, s);
+  }
+  ~PhaseTimer() {
+    if (on) {
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+  }
+};
+
 
 // Householder QR of a column-major m x n matrix A (lda).  Writes the
 // explicit thin factor Q (m x k, ldq) and R (k x n upper triangular, ldr),
@@ -49,6 +80,18 @@ int tri_inverse(cudaStream_t s, int k, const double* R, int64_t ldr, double* X);
 // (||Q1^T Q1 - I||_F > 1/4), in which case the caller falls back to Householder.
 int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
             double* R, int64_t ldr, int* ok);
+
+// Cheap no-truncation certificate for a tall column-major X (p x r, p >= r)
+// from its Gram matrix: G = X^T X = R^T R (blocked Cholesky), and
+//   sigma_min(X)^2 >= 1 / ||R^{-1}||_F^2 - 2 (p + r + 2) eps_mach ||X||_F^2
+// (the subtracted term bounds the rounding error of forming and factoring
+// G).  *ok_dev = 1 iff that lower bound exceeds
+// (1.25 max(delta, ||X||_F max(r, 2) eps_mach))^2, delta = *delta_dev *
+// delta_scale; 0 also when the Cholesky breaks down (caller falls back to a
+// QR-based certificate: the Gram route cannot resolve sigma_min below
+// ~sqrt(p eps_mach) ||X||).
+int gram_certificate(cudaStream_t s, int p, int r, const double* X, int64_t ldx,
+                     const double* delta_dev, double delta_scale, int* ok_dev);
 
 // Process-wide high-priority side stream used for look-ahead factorisation
 // of the next panel / diagonal block while the trailing update runs.

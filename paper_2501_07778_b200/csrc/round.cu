@@ -48,58 +48,48 @@ int fetch(cudaStream_t s, const T* dev, T* host) {
 }
 
 
-// QTT_ROUND_TRACE=1: synchronising per-phase timer (diagnostics only).
-struct PhaseTimer {
-  bool on;
-  cudaStream_t s;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  explicit PhaseTimer(cudaStream_t st) : on(getenv("QTT_ROUND_TRACE") != nullptr), s(st) {
-    if (on) {
-      cudaEventCreate(&e0);
-      cudaEventCreate(&e1);
-      cudaEventRecord(e0, s);
-    }
-  }
-  void lap(const char* what, int k, int a, int b, int c) {
-    if (!on) return;
-    cudaEventRecord(e1, s);
-    cudaEventSynchronize(e1);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    fprintf(stderr, "[round] %-10s k=%2d %5d x %5d (%5d) %8.3f ms\n", what, k, a, b, c, ms);
-    cudaEventRecord(e0, s);
-  }
-  ~PhaseTimer() {
-    if (on) {
-      cudaEventDestroy(e0);
-      cudaEventDestroy(e1);
-    }
-  }
-};
-
-// Right-to-left orthogonalisation of merged order-3 cores held in slots.
-// A core whose right unfolding is wide (n_k r_{k+1} < r_k) needs no QR: the
-// unfolding itself is the carry and the core becomes the identity, which is
-// right-orthonormal; the bond rank drops to its structural bound n_k r_{k+1}
-// exactly as the reference's QR would drop it (ttcore.py:296-306).
-int qr_sweep_right(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vector<int64_t>& n,
+// Right-to-left orthogonalisation of merged order-3 cores held in slots,
+// cores k = from .. 1.  A core whose right unfolding is wide or square
+// (n_k r_{k+1} <= r_k) needs no QR: the unfolding itself is the carry and the
+// core becomes the identity, which is right-orthonormal; the bond rank drops
+// to its structural bound n_k r_{k+1} exactly as the reference's QR would
+// drop it (ttcore.py:296-306).
+//
+// `zone` = number of leading cores that are exact identities (left
+// orthonormal, from reduce_left).  The sweep stops at the first TALL core
+// k <= zone: cores 0..k-1 are left-orthonormal identities and cores k+1..
+// right-orthonormal, so core k is the orthogonality centre and carries every
+// singular value of the bonds 1..k+1 (see round_slots).  Wide cores inside
+// the zone are folded into their (identity) left neighbour, which shrinks the
+// zone.  Returns the centre (0 when the sweep ran to the end); zone < 0
+// disables the early stop.
+int qr_sweep_right(cudaStream_t s, int from, std::vector<int64_t>& r, const std::vector<int64_t>& n,
                    const std::vector<int64_t>& off, double* work, double* tq, double* tr,
-                   double* tc) {
-  for (int k = d - 1; k >= 1; --k) {
+                   double* tc, int zone, int* centre) {
+  PhaseTimer pt(s);
+  *centre = 0;
+  for (int k = from; k >= 1; --k) {
     const int rows = (int)(n[k] * r[k + 1]);
     const int cols = (int)r[k];
     const int kk = std::min(rows, cols);
     const int prev = (int)(r[k - 1] * n[k - 1]);
-    if (rows < cols) {
+    if (k <= zone && rows > cols) {
+      *centre = k;
+      return kOk;
+    }
+    if (rows <= cols) {
       // M = I * M: prev_new (rows x prev) = M (rows x cols) * prev (cols x prev)
       QTT_TRY(dgemm(s, 0, 0, rows, prev, cols, 1.0, work + off[k], rows, work + off[k - 1], cols,
                     0.0, tc, rows));
       QTT_TRY(set_identity(s, rows, rows, work + off[k], rows));
+      pt.lap("rl-wide", k, rows, cols, prev);
     } else {
       QTT_TRY(qr(s, rows, cols, work + off[k], rows, tq, rows, tr, kk));
+      pt.lap("rl-qr", k, rows, cols, prev);
       QTT_CUDA(cudaMemcpyAsync(work + off[k], tq, sizeof(double) * rows * (int64_t)kk,
                                cudaMemcpyDeviceToDevice, s));
       QTT_TRY(dgemm(s, 0, 0, kk, prev, cols, 1.0, tr, kk, work + off[k - 1], cols, 0.0, tc, kk));
+      pt.lap("rl-carry", k, kk, prev, cols);
     }
     QTT_CUDA(cudaMemcpyAsync(work + off[k - 1], tc, sizeof(double) * kk * (int64_t)prev,
                              cudaMemcpyDeviceToDevice, s));
@@ -108,19 +98,21 @@ int qr_sweep_right(cudaStream_t s, int d, std::vector<int64_t>& r, const std::ve
   return kOk;
 }
 
-// Left structural reduction: wherever the left unfolding of core k is wide
-// (r_k n_k < r_{k+1}), multiply it into core k+1 and make core k the
-// identity.  Exact (no truncation decision; every bond is still examined by
-// the truncation sweep), and it removes the full-rank Householder/Cholesky
-// QRs the right-to-left sweep would otherwise spend on cores whose bond
-// ranks exceed the structural bound prod_{i<=k} n_i.
+// Left structural reduction: wherever the left unfolding of core k is wide or
+// square (r_k n_k <= r_{k+1}), multiply it into core k+1 and make core k the
+// identity.  Exact (no truncation decision; every bond is still certified or
+// examined by the truncation sweep), and it removes the full-rank
+// Householder/Cholesky QRs the right-to-left sweep would otherwise spend on
+// cores whose bond ranks exceed the structural bound prod_{i<=k} n_i.
+// *zone receives the number of LEADING cores that became identities.
 void reduce_left(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vector<int64_t>& n,
-                 const std::vector<int64_t>& off, double* work, double* tc, int* status) {
+                 const std::vector<int64_t>& off, double* work, double* tc, int* status, int* zone) {
   *status = kOk;
+  *zone = 0;
   for (int k = 0; k < d - 1; ++k) {
     const int m = (int)(r[k] * n[k]);
     const int N = (int)r[k + 1];
-    if (m >= N) continue;
+    if (m > N) continue;
     const int mc = (int)(n[k + 1] * r[k + 2]);
     double* core = work + off[k];
     double* next = work + off[k + 1];
@@ -133,12 +125,27 @@ void reduce_left(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vect
       return;
     }
     r[k + 1] = m;
+    if (*zone == k) *zone = k + 1;
   }
 }
 
 }  // namespace
 
 // Rounding core on merged order-3 slots (shared by qtt_round and the solver).
+//
+// Structure.  (1) reduce_left folds the structurally full-rank leading cores
+// into identities (left-orthonormal).  (2) The right-to-left QR sweep stops
+// at the first tall core c inside that zone: the TT is then orthogonal
+// around the centre c, whose right unfolding U_c (r_c x n_c r_{c+1}) holds
+// the singular values of bond c, and the unfolding of every bond b < c is a
+// reshape of the same data with r_b = r_{b+1} / n_b rows.  Its Gram matrix
+// is a sum of n_b principal submatrices of the Gram matrix of bond b+1, so
+// sigma_min(bond b)^2 >= n_b sigma_min(bond b+1)^2 (Cauchy interlacing):
+// ONE certificate on U_c, against the largest _chop threshold any of these
+// bonds can have, proves that none of the bonds 1..c truncates.  Their
+// cores stay identities and the truncation sweep starts at core c.  (3) If
+// that certificate fails the sweep is completed and every bond examined as
+// in the reference (ttcore.py:309-319).
 int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vector<int64_t>& n,
                 const std::vector<int64_t>& off, double* work, double eps) {
   if (d == 1) return kOk;
@@ -159,14 +166,40 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
   int* perm = reinterpret_cast<int*>(sc.p + 8 + maxcore);
   int* flags = reinterpret_cast<int*>(sc.p + 2);  // [0]: cert ok, [1]: rank
 
-  int st = kOk;
-  reduce_left(s, d, r, n, off, work, tc.p, &st);
+  int st = kOk, zone = 0, centre = 0;
+  PhaseTimer pt(s);
+  reduce_left(s, d, r, n, off, work, tc.p, &st, &zone);
   QTT_TRY(st);
-  QTT_TRY(qr_sweep_right(s, d, r, n, off, work, tq.p, tr.p, tc.p));
-  QTT_TRY(frob_norm(s, r[0] * n[0] * r[1], work + off[0], norm_dev));
+  pt.lap("reduce-left", zone, 0, 0, 0);
+  static const bool no_zone = getenv("QTT_ROUND_NO_ZONE") != nullptr;
+  if (no_zone) zone = -1;
+  QTT_TRY(qr_sweep_right(s, d - 1, r, n, off, work, tq.p, tr.p, tc.p, zone, &centre));
+  QTT_TRY(frob_norm(s, r[centre] * n[centre] * r[centre + 1], work + off[centre], norm_dev));
   const double dscale = eps / std::sqrt((double)std::max(d - 1, 1));
+  pt.lap("rl-sweep", centre, 0, 0, 0);
+  if (centre > 0) {
+    // bond `centre`: sigma_min of U_c, whose transpose is the column-major
+    // (n_c r_{c+1}) x r_c view of the core; tall by the stop rule
+    const int p = (int)(n[centre] * r[centre + 1]), rc = (int)r[centre];
+    int ok = 0;
+    QTT_TRY(gram_certificate(s, p, rc, work + off[centre], p, norm_dev, dscale, flags));
+    QTT_TRY(fetch(s, flags, &ok));
+    pt.lap("zone-gram", centre, p, rc, ok);
+    if (!ok) {
+      QTT_TRY(qr(s, p, rc, work + off[centre], p, nullptr, 1, tr.p, rc));
+      QTT_TRY(no_truncation_certificate(s, rc, tr.p, rc, norm_dev, dscale, flags));
+      QTT_TRY(fetch(s, flags, &ok));
+      pt.lap("zone-qr", centre, p, rc, ok);
+    }
+    if (!ok) {
+      int c2 = 0;
+      QTT_TRY(qr_sweep_right(s, centre, r, n, off, work, tq.p, tr.p, tc.p, -1, &c2));
+      QTT_TRY(frob_norm(s, r[0] * n[0] * r[1], work + off[0], norm_dev));
+      centre = 0;
+    }
+  }
 
-  for (int k = 0; k < d - 1; ++k) {
+  for (int k = centre; k < d - 1; ++k) {
     const int m = (int)(r[k] * n[k]);
     const int N = (int)r[k + 1];
     const int mc = (int)(n[k + 1] * r[k + 2]);  // rows of the next core's column-major view
@@ -177,9 +210,11 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
       // tall: L (m x N) row-major == core; factor its column-major copy
       QTT_TRY(transpose(s, N, m, core, N, lc.p, m));
       QTT_TRY(qr(s, m, N, lc.p, m, tq.p, m, tr.p, N));
+      pt.lap("lr-qr", k, m, N, mc);
       QTT_TRY(no_truncation_certificate(s, N, tr.p, N, norm_dev, dscale, flags));
       int ok = 0;
       QTT_TRY(fetch(s, flags, &ok));
+      pt.lap("lr-cert", k, N, N, ok);
       if (ok) {
         newk = N;
         QTT_TRY(transpose(s, m, N, tq.p, m, core, N));
@@ -218,6 +253,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
     }
     QTT_CUDA(cudaMemcpyAsync(next, tc.p, sizeof(double) * (int64_t)mc * newk,
                              cudaMemcpyDeviceToDevice, s));
+    pt.lap("lr-rest", k, m, N, newk);
     r[k + 1] = newk;
   }
   return kOk;
@@ -269,7 +305,8 @@ int norm_orth(const qtt_layout* in, const double* in_data, double* result, cudaS
   QTT_TRY(tc.alloc(s, maxcore));
   QTT_TRY(nb.alloc(s, 1));
   QTT_CUDA(cudaMemcpyAsync(work.p, in_data, sizeof(double) * total, cudaMemcpyDeviceToDevice, s));
-  QTT_TRY(qr_sweep_right(s, d, r, n, off, work.p, tq.p, tr.p, tc.p));
+  int centre = 0;
+  QTT_TRY(qr_sweep_right(s, d - 1, r, n, off, work.p, tq.p, tr.p, tc.p, -1, &centre));
   QTT_TRY(frob_norm(s, r[0] * n[0] * r[1], work.p + off[0], nb.p));
   return fetch(s, nb.p, result);
 }

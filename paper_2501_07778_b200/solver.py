@@ -126,16 +126,19 @@ class SolveOutcome:
 # ------------------------------------------------------------- residual
 
 
-def apply_tt_matrix(A: TTMatrix, v) -> torch.Tensor:
-    """Dense matvec of a TT operator on the device (solver.py:57-73)."""
+def apply_tt_matrix(A: TTMatrix, v):
+    """Dense matvec of a TT operator on the device (solver.py:57-73).  A host
+    array comes back as a host numpy array, as in the reference; a torch
+    tensor stays on the device."""
     dev = _lib.device()
-    x = v if isinstance(v, torch.Tensor) else torch.from_numpy(np.asarray(v, dtype=np.float64))
+    on_host = not isinstance(v, torch.Tensor)
+    x = v if not on_host else torch.from_numpy(np.ascontiguousarray(v, dtype=np.float64))
     x = x.to(device=dev, dtype=torch.float64).contiguous()
     out = torch.empty(A.shape[0], dtype=torch.float64, device=dev)
     lay = A._layout()
     _lib.call("qtt_dense_apply", ctypes.byref(lay), _lib.ptr(A.data), _lib.ptr(x), _lib.ptr(out),
               _lib.stream_handle())
-    return out
+    return out.cpu().numpy() if on_host else out
 
 
 def _apply_tt_to_tt(K: TTMatrix, u: TTVector) -> torch.Tensor:

@@ -147,7 +147,7 @@ def test_tt_ops_golden():
         assert abs(T.tt_norm(tx) - g[f"{name}_norm"]) <= 1e-13 * g[f"{name}_norm"]
         assert abs(T.tt_dot(tx, ty) - g[f"{name}_dot"]) <= 1e-12 * T.tt_norm(tx) * T.tt_norm(ty)
     out = S.apply_tt_matrix(T.TTMatrix(cases.apply_case()), g["apply_v"])
-    assert rel(out.cpu().numpy(), g["apply_out"]) < 1e-13
+    assert isinstance(out, np.ndarray) and rel(out, g["apply_out"]) < 1e-13
 
 
 @pytest.mark.parametrize("d", [3, 4])
