@@ -177,6 +177,289 @@ int chol_near_identity(cudaStream_t s, int n, double* G, int64_t ldg, double* U,
   return kOk;
 }
 
+
+// ---------------------------------------------------- small fused factor
+// Cholesky factor AND its inverse of an n x n Gram matrix, n <= 128, in ONE
+// CTA (the serial pivot chain of a small factorisation does not parallelise
+// across CTAs, and one launch replaces ~12: panels, updates, write-back,
+// diagonal inverses, doubling GEMMs).  G (upper triangle valid) = R^T R;
+// writes R and Ri = R^{-1} (both n x n upper, strictly lower part zeroed).
+// The matrix is handled as 2 x 2 blocks of 64: register factor of G11
+// (common.cuh), forward substitution for R12 with four lanes per column,
+// G22 - R12^T R12, register factor of R22, block inverses and
+// X12 = -X11 R12 X22.
+//
+// defect_mode (second CholeskyQR pass, G = Q1^T Q1): defect_out[0] receives
+// ||G - I||_F^2; if it is <= 1e-16 the factor is R = I + U, Ri = I - U with
+// U = strict upper part of E plus half its diagonal (error ||U||^2), with no
+// factorisation at all; above 1/16 (= (1/4)^2) the status flag is raised.
+// *status |= 1 on a non-positive pivot or a failed defect test (sticky:
+// speculative callers check it once per sweep).
+constexpr int kCisSmem = (5 * kBlk * (kBlk + 1) + 256 + kBlk + 16) * (int)sizeof(double);
+
+__device__ __forceinline__ double block_sum_256(double v, double* red) {
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) t += red[w];
+  return t;
+}
+
+typedef double (*CisBlk)[kBlk + 1];
+
+// Inverse of the upper-triangular 2 x 2 block matrix [S11 S12; 0 S22] held in
+// shared memory (identity padded): X11, X22 by register back substitution,
+// X12 = -X11 S12 X22.  Writes the inverse to Ri (n = kb1 + kb2; may be null)
+// and returns ||R^{-1}||_F^2 (of the unpadded n x n part).  S11 is
+// overwritten.  All 256 threads of the CTA must call.
+__device__ double cis_inverse(CisBlk S11, CisBlk S22, CisBlk S12, CisBlk X11, CisBlk X22, double* line,
+                              double* dinv, double* red, int kb1, int kb2, double* __restrict__ Ri,
+                              int64_t ldi) {
+  const int c = blk_col(), part = blk_part();
+  double a[16], x[16], y[16];
+  double nrm = 0.0;
+  blk_tri_inverse<false>(S11, x, y, line, dinv);
+  if (Ri) blk_store(x, Ri, ldi, kb1);
+#pragma unroll
+  for (int q = 0; q < 16; ++q)
+    if (part + 4 * q < kb1 && c < kb1) nrm = fma(x[q], x[q], nrm);
+  if (kb2 > 0) {
+    blk_to_smem(x, X11);
+    __syncthreads();
+    blk_tri_inverse<false>(S22, x, y, line, dinv);
+    blk_to_smem(x, X22);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = part + 4 * q;
+      if (i < kb2 && c < kb2) {
+        nrm = fma(x[q], x[q], nrm);
+        if (Ri) Ri[(kBlk + i) + (int64_t)(kBlk + c) * ldi] = x[q];
+      }
+    }
+    __syncthreads();
+    // T = S12 X22 (into S11, free now), X12 = -X11 T
+#pragma unroll
+    for (int q = 0; q < 16; ++q) a[q] = 0.0;
+    for (int k = 0; k <= c; ++k) {  // X22 upper triangular
+      const double xc = X22[k][c];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) a[q] = fma(S12[part + 4 * q][k], xc, a[q]);
+    }
+    __syncthreads();
+    blk_to_smem(a, S11);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) a[q] = 0.0;
+    for (int k = 0; k < kBlk; ++k) {
+      const double tc = -S11[k][c];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) a[q] = fma(X11[part + 4 * q][k], tc, a[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = part + 4 * q;
+      if (i < kb1 && c < kb2) {
+        nrm = fma(a[q], a[q], nrm);
+        if (Ri) Ri[i + (int64_t)(kBlk + c) * ldi] = a[q];
+      }
+    }
+  }
+  return block_sum_256(nrm, red);
+}
+
+__global__ void __launch_bounds__(256) chol_inv_small_kernel(int n, const double* __restrict__ G,
+                                                             int64_t ldg, double* __restrict__ R,
+                                                             int64_t ldr, double* __restrict__ Ri,
+                                                             int64_t ldi, int defect_mode,
+                                                             double* __restrict__ defect_out,
+                                                             int* __restrict__ status) {
+  extern __shared__ double cis_sm[];
+  typedef double (*Blk)[kBlk + 1];
+  Blk S11 = reinterpret_cast<Blk>(cis_sm);
+  Blk S22 = reinterpret_cast<Blk>(cis_sm + 1 * kBlk * (kBlk + 1));
+  Blk S12 = reinterpret_cast<Blk>(cis_sm + 2 * kBlk * (kBlk + 1));
+  Blk X11 = reinterpret_cast<Blk>(cis_sm + 3 * kBlk * (kBlk + 1));
+  Blk X22 = reinterpret_cast<Blk>(cis_sm + 4 * kBlk * (kBlk + 1));
+  double* line = cis_sm + 5 * kBlk * (kBlk + 1);
+  double* dinv = line + 256;
+  double* red = dinv + kBlk;
+  __shared__ int bad_s;
+  const int tid = threadIdx.x;
+  if (tid == 0) bad_s = 0;
+  const int kb1 = min(kBlk, n), kb2 = n - kb1;
+  const int c = blk_col(), part = blk_part(), lane = tid & 31;
+
+  if (defect_mode) {
+    double acc = 0.0;
+    for (int idx = tid; idx < n * n; idx += 256) {
+      const int i = idx % n, j = idx / n;
+      if (i > j) continue;
+      const double v = G[i + (int64_t)j * ldg] - (i == j ? 1.0 : 0.0);
+      acc = fma(i == j ? v : 2.0 * v, v, acc);
+    }
+    const double d2 = block_sum_256(acc, red);
+    if (tid == 0) {
+      defect_out[0] = d2;
+      defect_out[1] = (double)n;  // ||R2^{-1}||_F^2 on the shortcut path (R2 = I + O(delta))
+    }
+    if (!(d2 <= 0.0625)) {
+      if (tid == 0) atomicOr(status, 1);
+      return;
+    }
+    if (d2 <= 1e-16) {
+      for (int idx = tid; idx < n * n; idx += 256) {
+        const int i = idx % n, j = idx / n;
+        double u = 0.0;
+        if (i < j) u = G[i + (int64_t)j * ldg];
+        else if (i == j) u = 0.5 * (G[i + (int64_t)j * ldg] - 1.0);
+        const double e = (i == j) ? 1.0 : 0.0;
+        R[i + (int64_t)j * ldr] = e + u;
+        Ri[i + (int64_t)j * ldi] = e - u;
+      }
+      return;
+    }
+  }
+  __syncthreads();
+  if (defect_out && !defect_mode) {  // ||A||_F^2 = trace(G)
+    double tr = 0.0;
+    for (int i = tid; i < n; i += 256) tr += G[i + (int64_t)i * ldg];
+    tr = block_sum_256(tr, red);
+    if (tid == 0) defect_out[2] = tr;
+  }
+
+  // ---- R11
+  double a[16], x[16];
+  blk_load(a, G, ldg, kb1);
+  blk_factor<true>(a, line, &bad_s);
+  blk_to_smem(a, S11);
+  blk_store(a, R, ldr, kb1);
+  __syncthreads();
+  if (kb2 > 0) {
+    // ---- R12 = R11^{-T} G12 (column c of the second block column)
+    if (tid < kBlk) dinv[tid] = 1.0 / S11[tid][tid];
+    const bool act = c < kb2;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = part + 4 * q;
+      x[q] = (act && i < kb1) ? G[i + (int64_t)(kBlk + c) * ldg] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kBlk; ++j) {
+      const int qj = j >> 2, pj = j & 3;
+      const double v = x[qj] * dinv[j];
+      const double xj = -__shfl_sync(0xffffffffu, v, (lane & ~3) | pj);
+      const double* r = &S11[j][part];
+      if (part == pj) x[qj] = v;
+      if (part > pj) x[qj] = fma(r[4 * qj], xj, x[qj]);
+#pragma unroll
+      for (int q = qj + 1; q < 16; ++q) x[q] = fma(r[4 * q], xj, x[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = part + 4 * q;
+      S12[i][c] = x[q];
+      if (act && i < kb1) R[i + (int64_t)(kBlk + c) * ldr] = x[q];
+    }
+    __syncthreads();
+    // ---- G22 - R12^T R12 (identity padded), then R22
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = part + 4 * q;
+      a[q] = (i < kb2 && c < kb2) ? G[(kBlk + i) + (int64_t)(kBlk + c) * ldg] : (i == c ? 1.0 : 0.0);
+    }
+    for (int k = 0; k < kBlk; ++k) {
+      const double rc = -S12[k][c];
+      const double* rr = &S12[k][part];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) a[q] = fma(rr[4 * q], rc, a[q]);
+    }
+    __syncthreads();
+    blk_factor<true>(a, line, &bad_s);
+    blk_to_smem(a, S22);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int i = part + 4 * q;
+      if (i < kb2) {
+        if (c < kb2) R[(kBlk + i) + (int64_t)(kBlk + c) * ldr] = a[q];
+        Ri[(kBlk + i) + (int64_t)c * ldi] = 0.0;  // lower-left blocks (kb1 = 64 columns)
+        R[(kBlk + i) + (int64_t)c * ldr] = 0.0;
+      }
+    }
+    __syncthreads();
+  }
+  const double inv2 = cis_inverse(S11, S22, S12, X11, X22, line, dinv, red, kb1, kb2, Ri, ldi);
+  if (tid == 0 && defect_out) {
+    defect_out[1] = inv2;  // ||R^{-1}||_F^2
+  }
+  __syncthreads();
+  if (tid == 0 && bad_s) atomicOr(status, 1);
+}
+
+// No-truncation certificate for an upper-triangular R, k <= 128, in ONE CTA
+// (replaces the inverse + two norms + decision kernels, ~12 launches):
+// good iff 1 / ||R^{-1}||_F > 1.25 max(delta, ||R||_F max(k, 2) eps).
+// ok_dev (optional) receives the verdict; sflag (optional, sticky) gets bit 2
+// OR-ed in when the certificate fails (speculative sweeps).
+__global__ void __launch_bounds__(256) cert_small_kernel(int k, const double* __restrict__ R, int64_t ldr,
+                                                         const double* delta_dev, double delta_scale,
+                                                         int* ok_dev, int* sflag, int debug) {
+  extern __shared__ double cis_sm[];
+  CisBlk S11 = reinterpret_cast<CisBlk>(cis_sm);
+  CisBlk S22 = reinterpret_cast<CisBlk>(cis_sm + 1 * kBlk * (kBlk + 1));
+  CisBlk S12 = reinterpret_cast<CisBlk>(cis_sm + 2 * kBlk * (kBlk + 1));
+  CisBlk X11 = reinterpret_cast<CisBlk>(cis_sm + 3 * kBlk * (kBlk + 1));
+  CisBlk X22 = reinterpret_cast<CisBlk>(cis_sm + 4 * kBlk * (kBlk + 1));
+  double* line = cis_sm + 5 * kBlk * (kBlk + 1);
+  double* dinv = line + 256;
+  double* red = dinv + kBlk;
+  const int kb1 = min(kBlk, k), kb2 = k - kb1;
+  double rn = 0.0;
+  for (int idx = threadIdx.x; idx < kBlk * kBlk; idx += 256) {
+    const int i = idx % kBlk, c = idx / kBlk;
+    const double e = (i == c) ? 1.0 : 0.0;
+    const double v11 = (i < kb1 && c < kb1) ? (i <= c ? R[i + (int64_t)c * ldr] : 0.0) : e;
+    const double v12 = (i < kb1 && c < kb2) ? R[i + (int64_t)(kBlk + c) * ldr] : 0.0;
+    const double v22 = (i < kb2 && c < kb2) ? (i <= c ? R[(kBlk + i) + (int64_t)(kBlk + c) * ldr] : 0.0) : e;
+    S11[i][c] = v11;
+    S12[i][c] = v12;
+    S22[i][c] = v22;
+    if (i < kb1 && c < kb1) rn = fma(v11, v11, rn);
+    rn = fma(v12, v12, rn);
+    if (i < kb2 && c < kb2) rn = fma(v22, v22, rn);
+  }
+  rn = sqrt(block_sum_256(rn, red));
+  const double inv2 = cis_inverse(S11, S22, S12, X11, X22, line, dinv, red, kb1, kb2, nullptr, 0);
+  if (threadIdx.x == 0) {
+    const double eps = 2.220446049250313e-16;
+    const double xn = sqrt(inv2);
+    const double delta = delta_dev ? (*delta_dev) * delta_scale : 0.0;
+    const double thr = fmax(delta, rn * (double)max(k, 2) * eps);
+    const bool good = isfinite(xn) && isfinite(rn) && xn > 0.0 && (1.0 / xn) > 1.25 * thr;
+    if (ok_dev) *ok_dev = good ? 1 : 0;
+    if (sflag && !good) atomicOr(sflag, 2);
+    if (debug) printf("[cert-small] k=%d smin/||R||>=%.3e thr/||R||=%.3e good=%d\n", k, 1.0 / xn / rn,
+                      thr / rn, (int)good);
+  }
+}
+
+int chol_inv_small(cudaStream_t s, int n, const double* G, int64_t ldg, double* R, int64_t ldr,
+                   double* Ri, int64_t ldi, int defect_mode, double* defect_out, int* status) {
+  static DeviceFlag configured;
+  if (!configured.test()) {
+    QTT_CUDA(cudaFuncSetAttribute(chol_inv_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kCisSmem));
+    configured.set();
+  }
+  chol_inv_small_kernel<<<1, 256, kCisSmem, s>>>(n, G, ldg, R, ldr, Ri, ldi, defect_mode, defect_out,
+                                                status);
+  QTT_CHECK_LAUNCH();
+  return kOk;
+}
+
 // Blocked right-looking upper Cholesky G = R^T R (in place).  rblk: scratch
 // for the ceil(n/64) diagonal factors (64 x 64 each).
 //
@@ -264,6 +547,20 @@ __global__ void gram_certificate_kernel(int p, int r, const double* sc, const in
 
 }  // namespace
 
+int cert_small(cudaStream_t s, int k, const double* R, int64_t ldr, const double* delta_dev,
+               double delta_scale, int* ok_dev, int* sflag) {
+  if (k <= 0 || k > 2 * kBlk) return kInvalid;
+  static DeviceFlag configured;
+  if (!configured.test()) {
+    QTT_CUDA(cudaFuncSetAttribute(cert_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kCisSmem));
+    configured.set();
+  }
+  static const int debug = getenv("QTT_CERT_DEBUG") ? 1 : 0;
+  cert_small_kernel<<<1, 256, kCisSmem, s>>>(k, R, ldr, delta_dev, delta_scale, ok_dev, sflag, debug);
+  QTT_CHECK_LAUNCH();
+  return kOk;
+}
+
 int gram_certificate(cudaStream_t s, int p, int r, const double* X, int64_t ldx,
                      const double* delta_dev, double delta_scale, int* ok_dev) {
   if (p < r || r <= 0) return kInvalid;
@@ -296,6 +593,35 @@ int gram_certificate(cudaStream_t s, int p, int r, const double* X, int64_t ldx,
   return status;
 }
 
+// CholeskyQR2 of a small tall matrix (n <= 128) with NO host synchronisation:
+// Gram (DMMA) -> fused factor+inverse -> Q1 = A Ri1 -> Gram -> fused
+// factor+inverse with the near-identity shortcut -> Q = Q1 Ri2, R = R2 R1.
+// Seven launches.  Failure (pivot breakdown, ||Q1^T Q1 - I||_F > 1/4) raises
+// the sticky device flag *status and leaves unspecified output.
+int cholqr2_small(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
+                  double* R, int64_t ldr, int* status) {
+  if (m < n || n <= 0 || n > 2 * kBlk) return kInvalid;
+  const int64_t nn = n;
+  double *buf, *Q1;
+  QTT_CUDA(cudaMallocAsync(&buf, sizeof(double) * (4 * nn * nn + 8), s));
+  QTT_CUDA(cudaMallocAsync(&Q1, sizeof(double) * (int64_t)m * nn, s));
+  double *G = buf, *R1 = buf + nn * nn, *Ri = buf + 2 * nn * nn, *R2 = buf + 3 * nn * nn,
+         *sc = buf + 4 * nn * nn;
+  int status_code = kOk;
+  do {
+    if ((status_code = dgemm(s, 1, 0, n, n, m, 1.0, A, lda, A, lda, 0.0, G, nn, kGemmUpperC)) != kOk) break;
+    if ((status_code = chol_inv_small(s, n, G, nn, R1, nn, Ri, nn, 0, sc, status)) != kOk) break;
+    if ((status_code = dgemm(s, 0, 0, m, n, n, 1.0, A, lda, Ri, nn, 0.0, Q1, m, kGemmTriB)) != kOk) break;
+    if ((status_code = dgemm(s, 1, 0, n, n, m, 1.0, Q1, m, Q1, m, 0.0, G, nn, kGemmUpperC)) != kOk) break;
+    if ((status_code = chol_inv_small(s, n, G, nn, R2, nn, Ri, nn, 1, sc + 4, status)) != kOk) break;
+    if (Q && (status_code = dgemm(s, 0, 0, m, n, n, 1.0, Q1, m, Ri, nn, 0.0, Q, ldq, kGemmTriB)) != kOk) break;
+    if (R && (status_code = dgemm(s, 0, 0, n, n, n, 1.0, R2, nn, R1, nn, 0.0, R, ldr, kGemmTriA | kGemmTriB)) != kOk) break;
+  } while (false);
+  QTT_CUDA(cudaFreeAsync(buf, s));
+  QTT_CUDA(cudaFreeAsync(Q1, s));
+  return status_code;
+}
+
 int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
             double* R, int64_t ldr, int* ok) {
   *ok = 0;
@@ -313,17 +639,22 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
   QTT_CUDA(cudaMallocAsync(&bad, sizeof(int), s));
   QTT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
   int status = kOk;
+  PhaseTimer pt(s);
   do {
     // pass 1: G = A^T A = R1^T R1, Q1 = A R1^{-1}
     if ((status = dgemm(s, 1, 0, n, n, m, 1.0, A, lda, A, lda, 0.0, G, nn, kGemmUpperC)) != kOk) break;
+    pt.lap(" cq-gram1", 0, m, n, 0);
     if ((status = chol_upper(s, n, G, nn, rblk, bad)) != kOk) break;
     int hbad = 0;
     QTT_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
     QTT_CUDA(cudaStreamSynchronize(s));
     if (hbad) break;
+    pt.lap(" cq-chol1", 0, m, n, 0);
     QTT_CUDA(cudaMemcpyAsync(R1, G, sizeof(double) * nn * nn, cudaMemcpyDeviceToDevice, s));
     if ((status = tri_inverse(s, n, R1, nn, Ri)) != kOk) break;
+    pt.lap(" cq-inv1", 0, m, n, 0);
     if ((status = dgemm(s, 0, 0, m, n, n, 1.0, A, lda, Ri, nn, 0.0, Q1, m, kGemmTriB)) != kOk) break;
+    pt.lap(" cq-q1", 0, m, n, 0);
     // pass 2: certify cond(Q1) ~ 1, then G = Q1^T Q1 = R2^T R2, Q = Q1 R2^{-1}
     if ((status = dgemm(s, 1, 0, n, n, m, 1.0, Q1, m, Q1, m, 0.0, G, nn, kGemmUpperC)) != kOk) break;
     gram_defect_kernel<<<kDefectParts, 256, 0, s>>>(n, G, nn, parts);
@@ -335,6 +666,7 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
     QTT_CUDA(cudaStreamSynchronize(s));
     if (getenv("QTT_QR_DEBUG")) fprintf(stderr, "[cholqr2] m=%d n=%d defect=%.3e\n", m, n, std::sqrt(defect));
     const double delta = std::sqrt(defect);
+    pt.lap(" cq-gram2", 0, m, n, (int)(-std::log10(std::max(delta, 1e-99))));
     if (!(delta <= 0.25)) break;
     if (delta <= 1e-2 && !getenv("QTT_NO_NEAR_IDENTITY")) {
       int iters = 0;
@@ -352,10 +684,14 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
       QTT_CUDA(cudaStreamSynchronize(s));
       if (hbad) break;
     }
-    if ((status = tri_inverse(s, n, G, nn, Ri)) != kOk) break;
-    if ((status = dgemm(s, 0, 0, m, n, n, 1.0, Q1, m, Ri, nn, 0.0, Q, ldq, kGemmTriB)) != kOk) break;
+    pt.lap(" cq-chol2", 0, m, n, 0);
+    if (Q && (status = tri_inverse(s, n, G, nn, Ri)) != kOk) break;
+    pt.lap(" cq-inv2", 0, m, n, 0);
+    if (Q && (status = dgemm(s, 0, 0, m, n, n, 1.0, Q1, m, Ri, nn, 0.0, Q, ldq, kGemmTriB)) != kOk) break;
+    pt.lap(" cq-q", 0, m, n, 0);
     // R = R2 R1 (product of upper-triangular factors stays upper triangular)
     if ((status = dgemm(s, 0, 0, n, n, n, 1.0, G, nn, R1, nn, 0.0, R, ldr, kGemmTriA | kGemmTriB)) != kOk) break;
+    pt.lap(" cq-r", 0, m, n, 0);
     *ok = 1;
   } while (false);
   QTT_CUDA(cudaFreeAsync(G, s));

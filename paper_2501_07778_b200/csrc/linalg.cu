@@ -1389,7 +1389,8 @@ __device__ __forceinline__ void sq_reflect(double* sa, int m, int j, double* tau
 template <int E>
 __global__ void __launch_bounds__(SQ_THREADS) small_qr_kernel(int m, int n, const double* A,
                                                               int64_t lda, double* Q, int64_t ldq,
-                                                              double* R, int64_t ldr, int dbg) {
+                                                              double* R, int64_t ldr, int dbg,
+                                                              int sq_sleep) {
   extern __shared__ double sa[];  // m x n, ld m
   __shared__ double tau_s[SQ_MAXN];
   __shared__ int ready_s[SQ_MAXN];
@@ -1408,6 +1409,7 @@ __global__ void __launch_bounds__(SQ_THREADS) small_qr_kernel(int m, int n, cons
     const int jmax = min(c, k);
     for (int j = 0; j < jmax; ++j) {
       while (flag_acquire(ready + j) == 0) {
+        if (sq_sleep) __nanosleep(sq_sleep);
       }
       const double tj = tau_s[j];
       if (tj != 0.0) sq_apply(sa + (int64_t)j * m, col, tj, j, m, lane);
@@ -1494,31 +1496,44 @@ int small_qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double*
                                   SQ_MAXM * SQ_MAXN * 8));
     configured.set();
   }
+  static const int slp = getenv("QTT_SQR_SLEEP") ? atoi(getenv("QTT_SQR_SLEEP")) : 0;
   if (m <= 128)
-    small_qr_kernel<4><<<1, SQ_THREADS, smem, s>>>(m, n, A, lda, Q, ldq, R, ldr, dbg);
+    small_qr_kernel<4><<<1, SQ_THREADS, smem, s>>>(m, n, A, lda, Q, ldq, R, ldr, dbg, slp);
   else
-    small_qr_kernel<8><<<1, SQ_THREADS, smem, s>>>(m, n, A, lda, Q, ldq, R, ldr, dbg);
+    small_qr_kernel<8><<<1, SQ_THREADS, smem, s>>>(m, n, A, lda, Q, ldq, R, ldr, dbg, slp);
   QTT_CHECK_LAUNCH();
   return kOk;
 }
 
 int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
-       double* R, int64_t ldr) {
+       double* R, int64_t ldr, int* spec_dev, bool careful) {
   if (m <= 0 || n <= 0) return kInvalid;
   const int k = std::min(m, n);
   static const bool use_small = getenv("QTT_NO_SMALLQR") == nullptr;
+  // Small tall factors: sync-free CholeskyQR2 (7 launches) beats the serial
+  // Householder chain of small_qr from n = 32 on (75 / 155 us at n = 32 / 64).
+  static const bool use_cq_small = getenv("QTT_NO_CHOLQR_SMALL") == nullptr;
+  if (use_cq_small && !careful && m >= n && n >= 32 && n <= 128) {
+    if (spec_dev) return cholqr2_small(s, m, n, A, lda, Q, ldq, R, ldr, spec_dev);
+    int* st;
+    QTT_CUDA(cudaMallocAsync(&st, sizeof(int), s));
+    QTT_CUDA(cudaMemsetAsync(st, 0, sizeof(int), s));
+    QTT_TRY(cholqr2_small(s, m, n, A, lda, Q, ldq, R, ldr, st));
+    int hst = 0;
+    QTT_CUDA(cudaMemcpyAsync(&hst, st, sizeof(int), cudaMemcpyDeviceToHost, s));
+    QTT_CUDA(cudaStreamSynchronize(s));
+    QTT_CUDA(cudaFreeAsync(st, s));
+    if (!hst) return kOk;
+  }
   if (use_small && small_qr_fits(m, n)) return small_qr(s, m, n, A, lda, Q, ldq, R, ldr);
   // Large tall factors: try the GEMM-bound CholeskyQR2 first (certified, falls
   // back to Householder for ill-conditioned / rank-deficient inputs).
   static const bool use_chol = getenv("QTT_NO_CHOLQR") == nullptr;
   if (use_chol && m >= n && n >= 128) {
-    double* Qt = Q;
-    if (!Q) QTT_CUDA(cudaMallocAsync(&Qt, sizeof(double) * (int64_t)m * n, s));
     double* Rt = R;
     if (!R) QTT_CUDA(cudaMallocAsync(&Rt, sizeof(double) * (int64_t)n * n, s));
     int ok = 0;
-    QTT_TRY(cholqr2(s, m, n, A, lda, Qt, Q ? ldq : m, Rt, R ? ldr : n, &ok));
-    if (!Q) QTT_CUDA(cudaFreeAsync(Qt, s));
+    QTT_TRY(cholqr2(s, m, n, A, lda, Q, Q ? ldq : m, Rt, R ? ldr : n, &ok));  // Q may be null (R only)
     if (!R) QTT_CUDA(cudaFreeAsync(Rt, s));
     static const bool dbg = getenv("QTT_QR_DEBUG") != nullptr;
     if (dbg) fprintf(stderr, "[qr] cholqr2 m=%d n=%d %s\n", m, n, ok ? "ok" : "fallback");
@@ -1797,6 +1812,8 @@ int tri_inverse(cudaStream_t s, int k, const double* R, int64_t ldr, double* X) 
 
 int no_truncation_certificate(cudaStream_t s, int k, const double* R, int64_t ldr,
                               const double* delta_dev, double delta_scale, int* ok_dev) {
+  static const bool use_small = getenv("QTT_NO_CERT_SMALL") == nullptr;
+  if (use_small && k <= 2 * kBlk) return cert_small(s, k, R, ldr, delta_dev, delta_scale, ok_dev, nullptr);
   double *X, *norms;
   const int64_t kk = k;
   QTT_CUDA(cudaMallocAsync(&X, sizeof(double) * kk * kk, s));

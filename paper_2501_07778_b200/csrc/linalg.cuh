@@ -41,8 +41,16 @@ struct PhaseTimer {
 // factorised by one thread-block cluster (rows spread over up to 16 CTAs,
 // reductions through distributed shared memory), trailing updates and the
 // explicit-Q accumulation are compact-WY DMMA GEMMs.
+//
+// spec_dev (optional, device int): speculative mode.  Small well-conditioned
+// factors (32 <= n <= 128, m >= n) then run as CholeskyQR2 with no host
+// synchronisation; a breakdown ORs 1 into *spec_dev and leaves unspecified
+// output, and the caller redoes the call with careful = true (Householder /
+// synchronous CholeskyQR2 only) once it has read the flag.  Without spec_dev
+// the same path is used but checked (one synchronisation) and falls back
+// internally.
 int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
-       double* R, int64_t ldr);
+       double* R, int64_t ldr, int* spec_dev = nullptr, bool careful = false);
 
 // One-sided (Hestenes) Jacobi on the p x k column-major matrix X (ldx, in
 // place): X <- X W with W (k x k, ldw) orthogonal, so that the columns of X
@@ -69,6 +77,12 @@ int sort_chop(cudaStream_t s, int p, int k, const double* X, int64_t ldx, double
 int no_truncation_certificate(cudaStream_t s, int k, const double* R, int64_t ldr,
                               const double* delta_dev, double delta_scale, int* ok_dev);
 
+// The same certificate for k <= 128 in ONE single-CTA launch.  ok_dev
+// (optional) receives the verdict; sflag (optional) is a sticky device flag
+// that gets bit 2 OR-ed in on failure (speculative sweeps check it once).
+int cert_small(cudaStream_t s, int k, const double* R, int64_t ldr, const double* delta_dev,
+               double delta_scale, int* ok_dev, int* sflag);
+
 // X = R^{-1} for an upper-triangular k x k R (X: k x k, ld k): 64x64 diagonal
 // blocks inverted in shared memory, recursive doubling with DMMA GEMMs.
 int tri_inverse(cudaStream_t s, int k, const double* R, int64_t ldr, double* X);
@@ -92,6 +106,15 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
 // ~sqrt(p eps_mach) ||X||).
 int gram_certificate(cudaStream_t s, int p, int r, const double* X, int64_t ldx,
                      const double* delta_dev, double delta_scale, int* ok_dev);
+
+// CholeskyQR2 for n <= 128 without host synchronisation (seven launches, the
+// two n x n factorisations + inverses fused into one single-CTA kernel
+// each).  Q and/or R may be null.  On breakdown the sticky device flag
+// *status_dev is OR-ed with 1 and the outputs are unspecified: the caller
+// checks the flag at its next synchronisation point and redoes the
+// factorisation with qr(..., careful = true).
+int cholqr2_small(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
+                  double* R, int64_t ldr, int* status_dev);
 
 // Process-wide high-priority side stream used for look-ahead factorisation
 // of the next panel / diagonal block while the trailing update runs.

@@ -355,6 +355,31 @@ def test_qr_cholqr_path_and_fallback(cond):
     assert np.abs(q.T @ q - np.eye(n)).max() < 1e-12
 
 
+@pytest.mark.parametrize("m,n", [(256, 128), (200, 100), (96, 33), (128, 128), (130, 65), (512, 64)])
+@pytest.mark.parametrize("cond", [1e0, 1e4, 1e7, 1e13])
+def test_qr_small_cholqr_fused(m, n, cond):
+    """32 <= n <= 128 runs the sync-free CholeskyQR2 (Gram GEMMs + the fused
+    single-CTA factor/inverse kernel, 1 or 2 blocks of 64); ill-conditioned
+    inputs raise its status flag and fall back to Householder."""
+    from paper_2501_07778_b200 import _lib
+    import ctypes
+
+    rng = np.random.default_rng(m + 3 * n + int(np.log10(cond)))
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    a = (u * np.logspace(0, -np.log10(cond), n)) @ v.T
+    A = torch.tensor(a.ravel(order="F"), device="cuda")
+    Q = torch.zeros(m * n, dtype=torch.float64, device="cuda")
+    R = torch.full((n * n,), 7.0, dtype=torch.float64, device="cuda")
+    _lib.call("qtt_qr", ctypes.c_int64(m), ctypes.c_int64(n), _lib.ptr(A), ctypes.c_int64(m),
+              _lib.ptr(Q), ctypes.c_int64(m), _lib.ptr(R), ctypes.c_int64(n), _lib.stream_handle())
+    q = Q.cpu().numpy().reshape(n, m).T
+    r = R.cpu().numpy().reshape(n, n).T
+    assert np.abs(np.tril(r, -1)).max() == 0.0
+    assert np.linalg.norm(q @ r - a) <= 2e-13 * np.linalg.norm(a)
+    assert np.abs(q.T @ q - np.eye(n)).max() < 1e-12
+
+
 @pytest.mark.parametrize("m,n", [(128, 64), (64, 40), (300, 17)])
 def test_qr_small_rank_deficient(m, n):
     """Single-CTA QR with zero / repeated columns (tau = 0 reflectors)."""
