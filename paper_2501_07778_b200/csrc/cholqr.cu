@@ -446,6 +446,279 @@ __global__ void __launch_bounds__(256) cert_small_kernel(int k, const double* __
   }
 }
 
+// ------------------------------------------------ small fused factor, v2
+// Same contract as chol_inv_small_kernel, organised for latency: blocks of
+// 32, the matrix in shared memory (row stride 129), and each 32 x 32 diagonal
+// leaf factored AND inverted by ONE warp out of registers (lane l owns column
+// l; the pivot row travels through a double-buffered shared line, so a pivot
+// step costs one __syncwarp instead of a block barrier: ~180 cycles instead
+// of ~500).  Panels (R_kj = X_kk^T G_kj), trailing updates and the
+// off-diagonal inverse blocks (X_ij = -X_ii sum_k R_ik X_kj) are 32^3 block
+// products spread over the 8 warps with warp-uniform (broadcast) left
+// operands and branch-free, unrolled inner loops.  R lives in the upper
+// triangle of M, the off-diagonal blocks of X = R^{-1} transposed in the
+// lower block triangle, the diagonal blocks X_kk dense (zero below the
+// diagonal) in Xd.
+constexpr int kC2 = 32;             // block
+constexpr int kC2N = 128;           // max n
+constexpr int kC2Ld = kC2N + 1;     // row stride of M
+constexpr int kC2Xd = kC2 * (kC2 + 1);
+constexpr int kC2Smem =
+    (kC2N * kC2Ld + 4 * kC2Xd + 2 * kC2 + kC2Xd + 16) * (int)sizeof(double);
+
+// Factor + invert the 32 x 32 diagonal leaf at (k0, k0); executed by one warp.
+// R_kk -> upper triangle of M, X_kk -> xdk (32 x 33, zero below the diagonal).
+__device__ __forceinline__ void c2_leaf(double* M, double* xdk, double* rowbuf, int k0, int* bad) {
+  const int l = threadIdx.x & 31;
+  double col[kC2], dinv[kC2];
+#pragma unroll
+  for (int i = 0; i < kC2; ++i) col[i] = M[(k0 + i) * kC2Ld + k0 + l];
+#pragma unroll
+  for (int j = 0; j < kC2; ++j) {
+    const double p = __shfl_sync(0xffffffffu, col[j], j);
+    if (l == 0 && !(p > 0.0)) *bad = 1;
+    const double inv = rsqrt_nr(p);
+    dinv[j] = inv;
+    const double r = (l >= j) ? col[j] * inv : 0.0;
+    col[j] = r;
+    double* rb = rowbuf + (j & 1) * kC2;
+    rb[l] = r;
+    __syncwarp();
+#pragma unroll
+    for (int i = j + 1; i < kC2; ++i) col[i] = fma(-rb[i], r, col[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < kC2; ++i)
+    if (i <= l) M[(k0 + i) * kC2Ld + k0 + l] = col[i];
+  __syncwarp();
+  // column l of X = R^{-1}: v[i] accumulates sum_k R[i][k] x[k] until it becomes x[i]
+  double v[kC2];
+#pragma unroll
+  for (int i = 0; i < kC2; ++i) v[i] = 0.0;
+#pragma unroll
+  for (int k2 = kC2 - 1; k2 >= 0; --k2) {
+    const double xk = (l == k2) ? dinv[k2] : (l > k2 ? -v[k2] * dinv[k2] : 0.0);
+    v[k2] = xk;
+    const double* rcol = M + (size_t)k0 * kC2Ld + k0 + k2;  // R[i][k2], i < k2 (broadcast reads)
+#pragma unroll
+    for (int i = 0; i < k2; ++i) v[i] = fma(rcol[i * kC2Ld], xk, v[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < kC2; ++i) xdk[i * (kC2 + 1) + l] = v[i];  // zero for i > l
+}
+
+__global__ void __launch_bounds__(256) chol_inv_small2_kernel(int n, const double* __restrict__ G,
+                                                              int64_t ldg, double* __restrict__ R,
+                                                              int64_t ldr, double* __restrict__ Ri,
+                                                              int64_t ldi, int defect_mode,
+                                                              double* __restrict__ defect_out,
+                                                              int* __restrict__ status) {
+  extern __shared__ double c2_sm[];
+  double* M = c2_sm;
+  double* Xd = M + kC2N * kC2Ld;        // 4 dense diagonal blocks of X
+  double* rowbuf = Xd + 4 * kC2Xd;
+  double* T = rowbuf + 2 * kC2;         // 32 x 33
+  double* red = T + kC2Xd;
+  __shared__ int bad_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) bad_s = 0;
+  const int nb = (n + kC2 - 1) / kC2, np = nb * kC2;
+  const int dbg = defect_mode & 256;
+  defect_mode &= 255;
+  long long tstamp[16];
+  int nst = 0;
+  const long long t00 = clock64();
+#define C2_STAMP() do { if (dbg && tid == 0 && nst < 15) tstamp[nst++] = clock64() - t00; } while (0)
+
+  // load: thread -> (row i = tid & 127 within a column pair, columns j = tid >> 7 + 2 t)
+  // coalesced along i; all loads of a thread are independent (unrolled)
+  {
+    const int i = tid & (kC2N - 1), jh = tid >> 7;
+    double acc = 0.0, tr = 0.0;
+#pragma unroll 32
+    for (int t = 0; t < kC2N / 2; ++t) {
+      const int j = 2 * t + jh;
+      double v = 0.0;
+      if (i < n && j < n) v = G[i + (int64_t)j * ldg];
+      if (i > j) v = 0.0;
+      if (i == j) {
+        if (i >= n) v = 1.0;
+        else tr += v;
+      }
+      if (i < np && j < np) M[i * kC2Ld + j] = v;
+      if (i <= j && j < n) {
+        const double e = v - (i == j ? 1.0 : 0.0);
+        acc = fma(i == j ? e : 2.0 * e, e, acc);
+      }
+    }
+    tr = block_sum_256(tr, red);  // also the barrier after the load
+    if (tid == 0 && defect_out && !defect_mode) defect_out[2] = tr;
+    if (defect_mode) {
+      const double d2 = block_sum_256(acc, red);
+      if (tid == 0) {
+        defect_out[0] = d2;
+        defect_out[1] = (double)n;
+      }
+      if (!(d2 <= 0.0625)) {
+        if (tid == 0) atomicOr(status, 1);
+        return;
+      }
+      if (d2 <= 1e-16) {
+#pragma unroll 8
+        for (int t = 0; t < kC2N / 2; ++t) {
+          const int j = 2 * t + jh;
+          if (i < n && j < n) {
+            const double g = M[i * kC2Ld + j];  // upper triangle of G, zero below
+            const double e = (i == j) ? 1.0 : 0.0;
+            const double u = (i == j) ? 0.5 * (g - 1.0) : g;
+            R[i + (int64_t)j * ldr] = e + u;
+            Ri[i + (int64_t)j * ldi] = e - u;
+          }
+        }
+        return;
+      }
+    }
+  }
+  C2_STAMP();
+
+  const int c = lane, i0 = warp * 4;  // thread tile: rows i0..i0+3 of a block, column c
+  for (int kb = 0; kb < nb; ++kb) {
+    const int k0 = kb * kC2;
+    if (warp == 0) c2_leaf(M, Xd + kb * kC2Xd, rowbuf, k0, &bad_s);
+    __syncthreads();
+    C2_STAMP();
+    const int nj = nb - kb - 1;
+    if (nj == 0) break;
+    // panel: R[kb][jb] = X_kk^T G[kb][jb]; out[i][c] = sum_k X[k][i] G[k][c]
+    {
+      double out[3][4];
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) out[b][q] = 0.0;
+      const double* xk = Xd + kb * kC2Xd + i0;
+      const double* gk = M + (size_t)k0 * kC2Ld + k0 + kC2 + c;
+#pragma unroll 8
+      for (int k2 = 0; k2 < kC2; ++k2) {
+        const double x0 = xk[k2 * (kC2 + 1)], x1 = xk[k2 * (kC2 + 1) + 1], x2 = xk[k2 * (kC2 + 1) + 2],
+                     x3 = xk[k2 * (kC2 + 1) + 3];
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          if (b < nj) {
+            const double g = gk[k2 * kC2Ld + b * kC2];
+            out[b][0] = fma(x0, g, out[b][0]);
+            out[b][1] = fma(x1, g, out[b][1]);
+            out[b][2] = fma(x2, g, out[b][2]);
+            out[b][3] = fma(x3, g, out[b][3]);
+          }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+        if (b < nj)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) M[(k0 + i0 + q) * kC2Ld + k0 + (b + 1) * kC2 + c] = out[b][q];
+    }
+    __syncthreads();
+    // trailing update: G[ib][jb] -= R[kb][ib]^T R[kb][jb], kb < ib <= jb
+    for (int ib = kb + 1; ib < nb; ++ib)
+      for (int jb = ib; jb < nb; ++jb) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        const double* ri = M + (size_t)k0 * kC2Ld + ib * kC2 + i0;
+        const double* rj = M + (size_t)k0 * kC2Ld + jb * kC2 + c;
+#pragma unroll 8
+        for (int k2 = 0; k2 < kC2; ++k2) {
+          const double rc = rj[k2 * kC2Ld];
+          a0 = fma(ri[k2 * kC2Ld], rc, a0);
+          a1 = fma(ri[k2 * kC2Ld + 1], rc, a1);
+          a2 = fma(ri[k2 * kC2Ld + 2], rc, a2);
+          a3 = fma(ri[k2 * kC2Ld + 3], rc, a3);
+        }
+        double* dst = M + (size_t)(ib * kC2 + i0) * kC2Ld + jb * kC2 + c;
+        dst[0] -= a0;
+        dst[kC2Ld] -= a1;
+        dst[2 * kC2Ld] -= a2;
+        dst[3 * kC2Ld] -= a3;
+      }
+    __syncthreads();
+    C2_STAMP();
+  }
+  C2_STAMP();
+  // off-diagonal blocks of X = R^{-1}: X[ib][jb] = -X_ii sum_{kb=ib+1..jb} R[ib][kb] X[kb][jb];
+  // X[ib][jb][i][c] is stored at M[jb*32 + c][ib*32 + i]
+  for (int jb = 1; jb < nb; ++jb)
+    for (int ib = jb - 1; ib >= 0; --ib) {
+      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+      for (int kb = ib + 1; kb <= jb; ++kb) {
+        // X[kb*32 + k2][jb*32 + c]: dense diagonal block or transposed lower storage
+        const double* xp = (kb == jb) ? Xd + jb * kC2Xd + c : M + (size_t)(jb * kC2 + c) * kC2Ld + kb * kC2;
+        const int xs = (kb == jb) ? (kC2 + 1) : 1;
+        const double* rr = M + (size_t)(ib * kC2 + i0) * kC2Ld + kb * kC2;
+#pragma unroll 8
+        for (int k2 = 0; k2 < kC2; ++k2) {
+          const double xv = xp[k2 * xs];
+          t0 = fma(rr[k2], xv, t0);
+          t1 = fma(rr[kC2Ld + k2], xv, t1);
+          t2 = fma(rr[2 * kC2Ld + k2], xv, t2);
+          t3 = fma(rr[3 * kC2Ld + k2], xv, t3);
+        }
+      }
+      T[(i0 + 0) * (kC2 + 1) + c] = t0;
+      T[(i0 + 1) * (kC2 + 1) + c] = t1;
+      T[(i0 + 2) * (kC2 + 1) + c] = t2;
+      T[(i0 + 3) * (kC2 + 1) + c] = t3;
+      __syncthreads();
+      double x0 = 0.0, x1 = 0.0, x2 = 0.0, x3 = 0.0;
+      const double* xi = Xd + ib * kC2Xd + i0 * (kC2 + 1);  // X_ii[i][k2]
+#pragma unroll 8
+      for (int k2 = 0; k2 < kC2; ++k2) {
+        const double tv = T[k2 * (kC2 + 1) + c];
+        x0 = fma(xi[k2], tv, x0);
+        x1 = fma(xi[(kC2 + 1) + k2], tv, x1);
+        x2 = fma(xi[2 * (kC2 + 1) + k2], tv, x2);
+        x3 = fma(xi[3 * (kC2 + 1) + k2], tv, x3);
+      }
+      double* dst = M + (size_t)(jb * kC2 + c) * kC2Ld + ib * kC2 + i0;
+      dst[0] = -x0;
+      dst[1] = -x1;
+      dst[2] = -x2;
+      dst[3] = -x3;
+      __syncthreads();
+    }
+  C2_STAMP();
+  // write R, Ri (column-major, strictly lower zero) and ||Ri||_F^2
+  double nrm = 0.0;
+  {
+    const int i = tid & (kC2N - 1), jh = tid >> 7;
+#pragma unroll 16
+    for (int t = 0; t < kC2N / 2; ++t) {
+      const int j = 2 * t + jh;
+      if (i < n && j < n) {
+        const int ib = i >> 5, jb = j >> 5;
+        const double rv = (i <= j) ? M[i * kC2Ld + j] : 0.0;
+        double xv = 0.0;
+        if (ib == jb) xv = Xd[ib * kC2Xd + (i & 31) * (kC2 + 1) + (j & 31)];
+        else if (ib < jb) xv = M[j * kC2Ld + i];
+        R[i + (int64_t)j * ldr] = rv;
+        if (Ri) Ri[i + (int64_t)j * ldi] = xv;
+        nrm = fma(xv, xv, nrm);
+      }
+    }
+  }
+  nrm = block_sum_256(nrm, red);
+  if (tid == 0) {
+    if (defect_out) defect_out[1] = nrm;
+    if (bad_s) atomicOr(status, 1);
+    if (dbg) {
+      tstamp[nst++] = clock64() - t00;
+      printf("[cis2] n=%d stamps:", n);
+      for (int q = 0; q < nst; ++q) printf(" %lld", tstamp[q]);
+      printf("\n");
+    }
+  }
+#undef C2_STAMP
+}
+
 int chol_inv_small(cudaStream_t s, int n, const double* G, int64_t ldg, double* R, int64_t ldr,
                    double* Ri, int64_t ldi, int defect_mode, double* defect_out, int* status) {
   static DeviceFlag configured;
@@ -454,8 +727,21 @@ int chol_inv_small(cudaStream_t s, int n, const double* G, int64_t ldg, double* 
                                   kCisSmem));
     configured.set();
   }
-  chol_inv_small_kernel<<<1, 256, kCisSmem, s>>>(n, G, ldg, R, ldr, Ri, ldi, defect_mode, defect_out,
-                                                status);
+  static const bool v1 = getenv("QTT_CIS_V1") != nullptr;
+  if (v1) {
+    chol_inv_small_kernel<<<1, 256, kCisSmem, s>>>(n, G, ldg, R, ldr, Ri, ldi, defect_mode, defect_out,
+                                                  status);
+  } else {
+    static DeviceFlag configured2;
+    if (!configured2.test()) {
+      QTT_CUDA(cudaFuncSetAttribute(chol_inv_small2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kC2Smem));
+      configured2.set();
+    }
+    static const int dbg2 = getenv("QTT_CIS_DEBUG") ? 256 : 0;
+    chol_inv_small2_kernel<<<1, 256, kC2Smem, s>>>(n, G, ldg, R, ldr, Ri, ldi, defect_mode | dbg2, defect_out,
+                                                  status);
+  }
   QTT_CHECK_LAUNCH();
   return kOk;
 }
@@ -547,6 +833,31 @@ __global__ void gram_certificate_kernel(int p, int r, const double* sc, const in
 
 }  // namespace
 
+// Certificate from the by-products of cholqr2_small (sc[1] = ||R1^{-1}||_F^2,
+// sc[2] = ||A||_F^2, sc[4] = ||Q1^T Q1 - I||_F^2): R = R2 R1 with
+// sigma_min(R2)^2 = lambda_min(Q1^T Q1) >= 1 - delta, so
+// sigma_min(R) >= sqrt(1 - delta) / ||R1^{-1}||_F; ||R||_F = ||A||_F.
+__global__ void cert_factors_kernel(int k, const double* sc, const double* delta_dev, double delta_scale,
+                                    int* sflag, int debug) {
+  const double eps = 2.220446049250313e-16;
+  const double rn = sqrt(fmax(sc[2], 0.0));
+  const double lb = sqrt(fmax(1.0 - sqrt(fmax(sc[4], 0.0)), 0.0)) / sqrt(sc[1]);
+  const double delta = delta_dev ? (*delta_dev) * delta_scale : 0.0;
+  const double thr = fmax(delta, rn * (double)max(k, 2) * eps);
+  const bool good = isfinite(lb) && isfinite(rn) && lb > 1.25 * thr;
+  if (!good) atomicOr(sflag, 2);
+  if (debug) printf("[cert-factors] k=%d smin/||R||>=%.3e thr/||R||=%.3e good=%d\n", k, lb / rn, thr / rn,
+                    (int)good);
+}
+
+int cert_factors(cudaStream_t s, int k, const double* sc, const double* delta_dev, double delta_scale,
+                 int* sflag) {
+  static const int debug = getenv("QTT_CERT_DEBUG") ? 1 : 0;
+  cert_factors_kernel<<<1, 1, 0, s>>>(k, sc, delta_dev, delta_scale, sflag, debug);
+  QTT_CHECK_LAUNCH();
+  return kOk;
+}
+
 int cert_small(cudaStream_t s, int k, const double* R, int64_t ldr, const double* delta_dev,
                double delta_scale, int* ok_dev, int* sflag) {
   if (k <= 0 || k > 2 * kBlk) return kInvalid;
@@ -599,14 +910,14 @@ int gram_certificate(cudaStream_t s, int p, int r, const double* X, int64_t ldx,
 // Seven launches.  Failure (pivot breakdown, ||Q1^T Q1 - I||_F > 1/4) raises
 // the sticky device flag *status and leaves unspecified output.
 int cholqr2_small(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
-                  double* R, int64_t ldr, int* status) {
+                  double* R, int64_t ldr, int* status, double* scalars) {
   if (m < n || n <= 0 || n > 2 * kBlk) return kInvalid;
   const int64_t nn = n;
   double *buf, *Q1;
   QTT_CUDA(cudaMallocAsync(&buf, sizeof(double) * (4 * nn * nn + 8), s));
   QTT_CUDA(cudaMallocAsync(&Q1, sizeof(double) * (int64_t)m * nn, s));
   double *G = buf, *R1 = buf + nn * nn, *Ri = buf + 2 * nn * nn, *R2 = buf + 3 * nn * nn,
-         *sc = buf + 4 * nn * nn;
+         *sc = scalars ? scalars : buf + 4 * nn * nn;
   int status_code = kOk;
   do {
     if ((status_code = dgemm(s, 1, 0, n, n, m, 1.0, A, lda, A, lda, 0.0, G, nn, kGemmUpperC)) != kOk) break;

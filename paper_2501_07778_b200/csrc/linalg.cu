@@ -1513,7 +1513,7 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
   // Small tall factors: sync-free CholeskyQR2 (7 launches) beats the serial
   // Householder chain of small_qr from n = 32 on (75 / 155 us at n = 32 / 64).
   static const bool use_cq_small = getenv("QTT_NO_CHOLQR_SMALL") == nullptr;
-  if (use_cq_small && !careful && m >= n && n >= 32 && n <= 128) {
+  if (use_cq_small && !careful && m >= n && n >= kCholQrSmallMin && n <= kCholQrSmallMax) {
     if (spec_dev) return cholqr2_small(s, m, n, A, lda, Q, ldq, R, ldr, spec_dev);
     int* st;
     QTT_CUDA(cudaMallocAsync(&st, sizeof(int), s));

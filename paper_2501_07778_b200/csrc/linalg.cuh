@@ -113,8 +113,16 @@ int gram_certificate(cudaStream_t s, int p, int r, const double* X, int64_t ldx,
 // *status_dev is OR-ed with 1 and the outputs are unspecified: the caller
 // checks the flag at its next synchronisation point and redoes the
 // factorisation with qr(..., careful = true).
+//
+// scalars (optional, 8 device doubles) receives the by-products
+// [1] = ||R1^{-1}||_F^2, [2] = ||A||_F^2, [4] = ||Q1^T Q1 - I||_F^2, from which
+// cert_factors() evaluates the no-truncation certificate of R without
+// another pass (ORs 2 into the sticky flag when it fails).
 int cholqr2_small(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
-                  double* R, int64_t ldr, int* status_dev);
+                  double* R, int64_t ldr, int* status_dev, double* scalars = nullptr);
+int cert_factors(cudaStream_t s, int k, const double* scalars, const double* delta_dev,
+                 double delta_scale, int* sflag);
+constexpr int kCholQrSmallMin = 32, kCholQrSmallMax = 128;  // n range of cholqr2_small inside qr()
 
 // Process-wide high-priority side stream used for look-ahead factorisation
 // of the next panel / diagonal block while the trailing update runs.

@@ -138,6 +138,20 @@ void reduce_left(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vect
   }
 }
 
+// Speculative factorisation + no-truncation certificate of a tall A (m x n,
+// n <= kSpecMax): failures go to the sticky flag.
+int qr_cert_spec(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
+                 double* R, int64_t ldr, const double* norm_dev, double dscale, double* scalars,
+                 int* sflag) {
+  static const bool use_cq_small = getenv("QTT_NO_CHOLQR_SMALL") == nullptr;
+  if (use_cq_small && m >= n && n >= kCholQrSmallMin && n <= kCholQrSmallMax) {
+    QTT_TRY(cholqr2_small(s, m, n, A, lda, Q, ldq, R, ldr, sflag, scalars));
+    return cert_factors(s, n, scalars, norm_dev, dscale, sflag);
+  }
+  QTT_TRY(qr(s, m, n, A, lda, Q, ldq, R, ldr, sflag));
+  return cert_small(s, n, R, ldr, norm_dev, dscale, nullptr, sflag);
+}
+
 }  // namespace
 
 // Rounding core on merged order-3 slots (shared by qtt_round and the solver).
@@ -181,8 +195,8 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
   QTT_TRY(zp.alloc(s, maxcore));
   QTT_TRY(sc.alloc(s, 64 + 3 * maxcore));
   double* norm_dev = sc.p;
-  double* sigma = sc.p + 8;
-  int* perm = reinterpret_cast<int*>(sc.p + 8 + maxcore);
+  double* sigma = sc.p + 32;  // sc.p + 16 .. 23: by-products of cholqr2_small
+  int* perm = reinterpret_cast<int*>(sc.p + 32 + maxcore);
   int* flags = reinterpret_cast<int*>(sc.p + 2);  // [0]: cert ok, [1]: rank, [2]: sticky spec flag
   int* sflag = spec_failed ? flags + 2 : nullptr;
   if (sflag) QTT_CUDA(cudaMemsetAsync(sflag, 0, sizeof(int), s));
@@ -211,8 +225,8 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
     const int p = (int)(n[centre] * r[centre + 1]), rc = (int)r[centre];
     int ok = 0;
     if (sflag && rc <= kSpecMax) {
-      QTT_TRY(qr(s, p, rc, work + off[centre], p, nullptr, 1, tr.p, rc, sflag));
-      QTT_TRY(cert_small(s, rc, tr.p, rc, norm_dev, dscale, nullptr, sflag));
+      QTT_TRY(qr_cert_spec(s, p, rc, work + off[centre], p, nullptr, 1, tr.p, rc, norm_dev, dscale,
+                           sc.p + 16, sflag));
       ok = 1;  // verified through the sticky flag
       pt.lap("zone-spec", centre, p, rc, ok);
     } else {
@@ -259,8 +273,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
       QTT_TRY(transpose(s, N, m, core, N, lc.p, m));
       int ok = 0;
       if (sflag && N <= kSpecMax) {
-        QTT_TRY(qr(s, m, N, lc.p, m, tq.p, m, tr.p, N, sflag));
-        QTT_TRY(cert_small(s, N, tr.p, N, norm_dev, dscale, nullptr, sflag));
+        QTT_TRY(qr_cert_spec(s, m, N, lc.p, m, tq.p, m, tr.p, N, norm_dev, dscale, sc.p + 16, sflag));
         ok = 1;  // verified through the sticky flag
         pt.lap("lr-spec", k, m, N, mc);
       } else {
@@ -296,8 +309,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
       // wide: L^T (N x m) column-major == core memory
       int ok = 0;
       if (sflag && m <= kSpecMax) {
-        QTT_TRY(qr(s, N, m, core, N, nullptr, 1, tr.p, m, sflag));
-        QTT_TRY(cert_small(s, m, tr.p, m, norm_dev, dscale, nullptr, sflag));
+        QTT_TRY(qr_cert_spec(s, N, m, core, N, nullptr, 1, tr.p, m, norm_dev, dscale, sc.p + 16, sflag));
         ok = 1;
       } else {
         int bad = 0;
