@@ -192,7 +192,18 @@ def run_concurrent(jobs):
     if _POOL is None:
         _POOL = concurrent.futures.ThreadPoolExecutor(max_workers=12, thread_name_prefix="qtt-chain")
     if len(_STREAMS) < len(jobs) or _STREAMS[0].device.index != dev:
-        _STREAMS = [torch.cuda.Stream(device=dev) for _ in range(max(12, len(jobs)))]
+        # callers order their jobs longest first: the earlier a chain, the
+        # higher its stream priority, so the critical (longest) chain is not
+        # queued behind the short chains' kernels (QTT_CHAIN_PRIORITY=0: flat)
+        levels = 1
+        if os.environ.get("QTT_CHAIN_PRIORITY", "1") != "0":
+            try:
+                lo, hi = torch.cuda.Stream.priority_range()  # (least, greatest), e.g. (0, -5)
+                levels = abs(hi - lo) + 1
+            except Exception:
+                levels = 2
+        _STREAMS = [torch.cuda.Stream(device=dev, priority=-max(levels - 1 - i, 0))
+                    for i in range(max(12, len(jobs)))]
     main = torch.cuda.current_stream()
 
     def run(fn, arg, stream):

@@ -933,9 +933,21 @@ int cholqr2_small(cudaStream_t s, int m, int n, const double* A, int64_t lda, do
   return status_code;
 }
 
+// Ri <- 2 I - G on the upper triangle (zero below): inverse of G = I + U to
+// first order, exact to ||U||^2.
+__global__ void neumann1_kernel(int n, const double* __restrict__ G, int64_t ldg,
+                                double* __restrict__ Ri, int64_t ldi) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx % n), c = (int)(idx / n);
+    Ri[r + (int64_t)c * ldi] = (r > c) ? 0.0 : ((r == c ? 2.0 : 0.0) - G[r + (int64_t)c * ldg]);
+  }
+}
+
 int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
-            double* R, int64_t ldr, int* ok) {
+            double* R, int64_t ldr, int* ok, QrInfo* info) {
   *ok = 0;
+  if (info) info->valid = false;
   if (m < n || n <= 0) return kOk;
   const int64_t nn = n;
   double *G, *R1, *Ri, *Q1, *rblk, *scal, *parts;
@@ -954,15 +966,16 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
   do {
     // pass 1: G = A^T A = R1^T R1, Q1 = A R1^{-1}
     if ((status = dgemm(s, 1, 0, n, n, m, 1.0, A, lda, A, lda, 0.0, G, nn, kGemmUpperC)) != kOk) break;
+    gram_trace_kernel<<<1, 256, 0, s>>>(n, G, nn, scal + 1);  // ||A||_F^2
+    QTT_CHECK_LAUNCH();
     pt.lap(" cq-gram1", 0, m, n, 0);
     if ((status = chol_upper(s, n, G, nn, rblk, bad)) != kOk) break;
-    int hbad = 0;
-    QTT_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
-    QTT_CUDA(cudaStreamSynchronize(s));
-    if (hbad) break;
     pt.lap(" cq-chol1", 0, m, n, 0);
+    // no synchronisation here: a breakdown (bad pivot -> NaN) surfaces in the
+    // defect below, which is read together with the flag
     QTT_CUDA(cudaMemcpyAsync(R1, G, sizeof(double) * nn * nn, cudaMemcpyDeviceToDevice, s));
     if ((status = tri_inverse(s, n, R1, nn, Ri)) != kOk) break;
+    if ((status = frob_norm(s, nn * nn, Ri, scal + 2)) != kOk) break;  // ||R1^{-1}||_F
     pt.lap(" cq-inv1", 0, m, n, 0);
     if ((status = dgemm(s, 0, 0, m, n, n, 1.0, A, lda, Ri, nn, 0.0, Q1, m, kGemmTriB)) != kOk) break;
     pt.lap(" cq-q1", 0, m, n, 0);
@@ -972,13 +985,17 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
     QTT_CHECK_LAUNCH();
     sum_parts_kernel<<<1, 32, 0, s>>>(kDefectParts, parts, scal);
     QTT_CHECK_LAUNCH();
-    double defect = 0.0;
-    QTT_CUDA(cudaMemcpyAsync(&defect, scal, sizeof(double), cudaMemcpyDeviceToHost, s));
+    double hs[3] = {0.0, 0.0, 0.0};  // defect^2, ||A||_F^2, ||R1^{-1}||_F
+    int hbad = 0;
+    QTT_CUDA(cudaMemcpyAsync(hs, scal, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    QTT_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
     QTT_CUDA(cudaStreamSynchronize(s));
+    const double defect = hs[0];
     if (getenv("QTT_QR_DEBUG")) fprintf(stderr, "[cholqr2] m=%d n=%d defect=%.3e\n", m, n, std::sqrt(defect));
     const double delta = std::sqrt(defect);
     pt.lap(" cq-gram2", 0, m, n, (int)(-std::log10(std::max(delta, 1e-99))));
-    if (!(delta <= 0.25)) break;
+    if (hbad || !(delta <= 0.25)) break;
+    bool near_id = false;
     if (delta <= 1e-2 && !getenv("QTT_NO_NEAR_IDENTITY")) {
       int iters = 0;
       while (iters < 8 && std::pow(std::max(delta, 1e-300), iters + 2) > 1e-17) ++iters;
@@ -989,6 +1006,7 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
       QTT_CUDA(cudaFreeAsync(U, s));
       QTT_CUDA(cudaFreeAsync(W, s));
       if (status != kOk) break;
+      near_id = true;
     } else {
       if ((status = chol_upper(s, n, G, nn, rblk, bad)) != kOk) break;
       QTT_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -996,7 +1014,16 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
       if (hbad) break;
     }
     pt.lap(" cq-chol2", 0, m, n, 0);
-    if (Q && (status = tri_inverse(s, n, G, nn, Ri)) != kOk) break;
+    if (Q) {
+      if (near_id && delta <= 1e-9) {
+        // R2 = I + U with ||U|| <= delta: R2^{-1} = I - U to delta^2 <= 1e-18
+        const int blocks = (int)std::min<int64_t>(ceil_div(nn * nn, 256), 8 * num_sms());
+        neumann1_kernel<<<blocks, 256, 0, s>>>(n, G, nn, Ri, nn);
+        QTT_CHECK_LAUNCH();
+      } else if ((status = tri_inverse(s, n, G, nn, Ri)) != kOk) {
+        break;
+      }
+    }
     pt.lap(" cq-inv2", 0, m, n, 0);
     if (Q && (status = dgemm(s, 0, 0, m, n, n, 1.0, Q1, m, Ri, nn, 0.0, Q, ldq, kGemmTriB)) != kOk) break;
     pt.lap(" cq-q", 0, m, n, 0);
@@ -1004,6 +1031,12 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
     if ((status = dgemm(s, 0, 0, n, n, n, 1.0, G, nn, R1, nn, 0.0, R, ldr, kGemmTriA | kGemmTriB)) != kOk) break;
     pt.lap(" cq-r", 0, m, n, 0);
     *ok = 1;
+    if (info) {
+      // sigma_min(R) >= sigma_min(R2) sigma_min(R1) >= sqrt(1 - delta) / ||R1^{-1}||_F
+      info->valid = std::isfinite(hs[2]) && hs[2] > 0.0 && std::isfinite(hs[1]);
+      info->sigma_lb = std::sqrt(std::max(1.0 - delta, 0.0)) / hs[2];
+      info->anorm = std::sqrt(std::max(hs[1], 0.0));
+    }
   } while (false);
   QTT_CUDA(cudaFreeAsync(G, s));
   QTT_CUDA(cudaFreeAsync(R1, s));

@@ -1506,7 +1506,8 @@ int small_qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double*
 }
 
 int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
-       double* R, int64_t ldr, int* spec_dev, bool careful) {
+       double* R, int64_t ldr, int* spec_dev, bool careful, QrInfo* info) {
+  if (info) info->valid = false;
   if (m <= 0 || n <= 0) return kInvalid;
   const int k = std::min(m, n);
   static const bool use_small = getenv("QTT_NO_SMALLQR") == nullptr;
@@ -1533,7 +1534,7 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
     double* Rt = R;
     if (!R) QTT_CUDA(cudaMallocAsync(&Rt, sizeof(double) * (int64_t)n * n, s));
     int ok = 0;
-    QTT_TRY(cholqr2(s, m, n, A, lda, Q, Q ? ldq : m, Rt, R ? ldr : n, &ok));  // Q may be null (R only)
+    QTT_TRY(cholqr2(s, m, n, A, lda, Q, Q ? ldq : m, Rt, R ? ldr : n, &ok, info));  // Q may be null (R only)
     if (!R) QTT_CUDA(cudaFreeAsync(Rt, s));
     static const bool dbg = getenv("QTT_QR_DEBUG") != nullptr;
     if (dbg) fprintf(stderr, "[qr] cholqr2 m=%d n=%d %s\n", m, n, ok ? "ok" : "fallback");

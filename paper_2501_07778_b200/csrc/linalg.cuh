@@ -49,8 +49,9 @@ struct PhaseTimer {
 // synchronous CholeskyQR2 only) once it has read the flag.  Without spec_dev
 // the same path is used but checked (one synchronisation) and falls back
 // internally.
+struct QrInfo;
 int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
-       double* R, int64_t ldr, int* spec_dev = nullptr, bool careful = false);
+       double* R, int64_t ldr, int* spec_dev = nullptr, bool careful = false, QrInfo* info = nullptr);
 
 // One-sided (Hestenes) Jacobi on the p x k column-major matrix X (ldx, in
 // place): X <- X W with W (k x k, ldw) orthogonal, so that the columns of X
@@ -92,8 +93,16 @@ int tri_inverse(cudaStream_t s, int k, const double* R, int64_t ldr, double* X);
 // tall matrices.  Returns kOk and sets *ok = 1 on success; *ok = 0 when the
 // Cholesky breaks down or the first-pass Q is too far from orthonormal
 // (||Q1^T Q1 - I||_F > 1/4), in which case the caller falls back to Householder.
+// info (optional): on success, a lower bound of sigma_min(R) and ||R||_F =
+// ||A||_F from the factorisation's own by-products, so the caller can decide
+// the no-truncation certificate on the host without another pass.
+struct QrInfo {
+  bool valid = false;
+  double sigma_lb = 0.0;  // sigma_min(R) >= sigma_lb
+  double anorm = 0.0;     // ||A||_F = ||R||_F
+};
 int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
-            double* R, int64_t ldr, int* ok);
+            double* R, int64_t ldr, int* ok, QrInfo* info = nullptr);
 
 // Cheap no-truncation certificate for a tall column-major X (p x r, p >= r)
 // from its Gram matrix: G = X^T X = R^T R (blocked Cholesky), and

@@ -138,6 +138,13 @@ void reduce_left(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vect
   }
 }
 
+// Host-side certificate from the by-products of a synchronous CholeskyQR2
+// (same inequality as certificate_kernel in linalg.cu).
+bool host_certificate(const QrInfo& qi, int k, double delta) {
+  const double thr = std::max(delta, qi.anorm * std::max(k, 2) * 2.220446049250313e-16);
+  return qi.valid && std::isfinite(qi.sigma_lb) && qi.sigma_lb > 1.25 * thr;
+}
+
 // Speculative factorisation + no-truncation certificate of a tall A (m x n,
 // n <= kSpecMax): failures go to the sticky flag.
 int qr_cert_spec(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, int64_t ldq,
@@ -219,6 +226,12 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
   QTT_TRY(frob_norm(s, r[centre] * n[centre] * r[centre + 1], work + off[centre], norm_dev));
   const double dscale = eps / std::sqrt((double)std::max(d - 1, 1));
   pt.lap("rl-sweep", centre, 0, 0, 0);
+  double norm_host = -1.0;  // fetched on first use by a host-side certificate
+  auto host_delta = [&](double* out) -> int {
+    if (norm_host < 0.0) QTT_TRY(fetch(s, norm_dev, &norm_host));
+    *out = norm_host * dscale;
+    return kOk;
+  };
   if (centre > 0) {
     // bond `centre`: sigma_min of U_c, whose transpose is the column-major
     // (n_c r_{c+1}) x r_c view of the core; tall by the stop rule
@@ -243,9 +256,16 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
         pt.lap("zone-gram", centre, p, rc, ok);
       }
       if (!ok) {
-        QTT_TRY(qr(s, p, rc, work + off[centre], p, nullptr, 1, tr.p, rc));
-        QTT_TRY(no_truncation_certificate(s, rc, tr.p, rc, norm_dev, dscale, flags));
-        QTT_TRY(fetch(s, flags, &ok));
+        QrInfo qi;
+        double hd = 0.0;
+        QTT_TRY(qr(s, p, rc, work + off[centre], p, nullptr, 1, tr.p, rc, nullptr, false, &qi));
+        if (qi.valid) QTT_TRY(host_delta(&hd));
+        if (qi.valid && host_certificate(qi, rc, hd)) {
+          ok = 1;
+        } else {
+          QTT_TRY(no_truncation_certificate(s, rc, tr.p, rc, norm_dev, dscale, flags));
+          QTT_TRY(fetch(s, flags, &ok));
+        }
         pt.lap("zone-qr", centre, p, rc, ok);
       }
     }
@@ -257,6 +277,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
       int c2 = 0;
       QTT_TRY(qr_sweep_right(s, centre, r, n, off, work, tq.p, tr.p, tc.p, -1, &c2));
       QTT_TRY(frob_norm(s, r[0] * n[0] * r[1], work + off[0], norm_dev));
+      norm_host = -1.0;
       centre = 0;
     }
   }
@@ -280,10 +301,17 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
         int bad = 0;
         QTT_TRY(spec_bad(&bad));
         if (bad) return kOk;
-        QTT_TRY(qr(s, m, N, lc.p, m, tq.p, m, tr.p, N));
+        QrInfo qi;
+        double hd = 0.0;
+        QTT_TRY(qr(s, m, N, lc.p, m, tq.p, m, tr.p, N, nullptr, false, &qi));
         pt.lap("lr-qr", k, m, N, mc);
-        QTT_TRY(no_truncation_certificate(s, N, tr.p, N, norm_dev, dscale, flags));
-        QTT_TRY(fetch(s, flags, &ok));
+        if (qi.valid) QTT_TRY(host_delta(&hd));
+        if (qi.valid && host_certificate(qi, N, hd)) {
+          ok = 1;  // decided from the factorisation's by-products, no extra pass
+        } else {
+          QTT_TRY(no_truncation_certificate(s, N, tr.p, N, norm_dev, dscale, flags));
+          QTT_TRY(fetch(s, flags, &ok));
+        }
         pt.lap("lr-cert", k, N, N, ok);
       }
       if (!ok && sflag) {
@@ -315,9 +343,16 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
         int bad = 0;
         QTT_TRY(spec_bad(&bad));
         if (bad) return kOk;
-        QTT_TRY(qr(s, N, m, core, N, nullptr, 1, tr.p, m));
-        QTT_TRY(no_truncation_certificate(s, m, tr.p, m, norm_dev, dscale, flags));
-        QTT_TRY(fetch(s, flags, &ok));
+        QrInfo qi;
+        double hd = 0.0;
+        QTT_TRY(qr(s, N, m, core, N, nullptr, 1, tr.p, m, nullptr, false, &qi));
+        if (qi.valid) QTT_TRY(host_delta(&hd));
+        if (qi.valid && host_certificate(qi, m, hd)) {
+          ok = 1;
+        } else {
+          QTT_TRY(no_truncation_certificate(s, m, tr.p, m, norm_dev, dscale, flags));
+          QTT_TRY(fetch(s, flags, &ok));
+        }
       }
       if (!ok && sflag) {
         *spec_failed = 1;
