@@ -232,20 +232,25 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
     *out = norm_host * dscale;
     return kOk;
   };
+  // Speculation continues past this point only while certificates pass: the
+  // sweep above is plain orthogonalisation (valid whether or not bonds
+  // truncate), so once its factorisations are known to be sound (one flag
+  // read) the FIRST certificates are examined synchronously; a truncating
+  // rounding (assembly, coupling, solver) then simply carries on on the
+  // examined path with nothing wasted, and a full-rank one runs the
+  // remaining bonds without host round trips.
+  bool spec_lr = sflag != nullptr;
+  if (sflag) {
+    int bad = 0;
+    QTT_TRY(spec_bad(&bad));
+    if (bad) return kOk;
+  }
   if (centre > 0) {
     // bond `centre`: sigma_min of U_c, whose transpose is the column-major
     // (n_c r_{c+1}) x r_c view of the core; tall by the stop rule
     const int p = (int)(n[centre] * r[centre + 1]), rc = (int)r[centre];
     int ok = 0;
-    if (sflag && rc <= kSpecMax) {
-      QTT_TRY(qr_cert_spec(s, p, rc, work + off[centre], p, nullptr, 1, tr.p, rc, norm_dev, dscale,
-                           sc.p + 16, sflag));
-      ok = 1;  // verified through the sticky flag
-      pt.lap("zone-spec", centre, p, rc, ok);
-    } else {
-      int bad = 0;
-      QTT_TRY(spec_bad(&bad));
-      if (bad) return kOk;
+    {
       static const bool try_gram = getenv("QTT_ZONE_GRAM") != nullptr;
       if (try_gram) {
         // cheap Gram route: resolves sigma_min only down to ~1e-6 ||U_c||,
@@ -270,10 +275,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
       }
     }
     if (!ok) {
-      if (sflag) {  // a truncating bond: not a speculative case
-        *spec_failed = 1;
-        return kOk;
-      }
+      spec_lr = false;
       int c2 = 0;
       QTT_TRY(qr_sweep_right(s, centre, r, n, off, work, tq.p, tr.p, tc.p, -1, &c2));
       QTT_TRY(frob_norm(s, r[0] * n[0] * r[1], work + off[0], norm_dev));
@@ -282,7 +284,9 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
     }
   }
 
+  const int first_bond = centre;
   for (int k = centre; k < d - 1; ++k) {
+    const bool spec_k = spec_lr && k > first_bond;  // the first bond is examined
     const int m = (int)(r[k] * n[k]);
     const int N = (int)r[k + 1];
     const int mc = (int)(n[k + 1] * r[k + 2]);  // rows of the next core's column-major view
@@ -293,14 +297,16 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
       // tall: L (m x N) row-major == core; factor its column-major copy
       QTT_TRY(transpose(s, N, m, core, N, lc.p, m));
       int ok = 0;
-      if (sflag && N <= kSpecMax) {
+      if (spec_k && N <= kSpecMax) {
         QTT_TRY(qr_cert_spec(s, m, N, lc.p, m, tq.p, m, tr.p, N, norm_dev, dscale, sc.p + 16, sflag));
         ok = 1;  // verified through the sticky flag
         pt.lap("lr-spec", k, m, N, mc);
       } else {
-        int bad = 0;
-        QTT_TRY(spec_bad(&bad));
-        if (bad) return kOk;
+        if (spec_k) {
+          int bad = 0;
+          QTT_TRY(spec_bad(&bad));
+          if (bad) return kOk;
+        }
         QrInfo qi;
         double hd = 0.0;
         QTT_TRY(qr(s, m, N, lc.p, m, tq.p, m, tr.p, N, nullptr, false, &qi));
@@ -314,10 +320,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
         }
         pt.lap("lr-cert", k, N, N, ok);
       }
-      if (!ok && sflag) {
-        *spec_failed = 1;
-        return kOk;
-      }
+      if (!ok) spec_lr = false;  // examined bond (earlier speculative ones were just verified)
       if (ok) {
         newk = N;
         QTT_TRY(transpose(s, m, N, tq.p, m, core, N));
@@ -336,13 +339,15 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
     } else {
       // wide: L^T (N x m) column-major == core memory
       int ok = 0;
-      if (sflag && m <= kSpecMax) {
+      if (spec_k && m <= kSpecMax) {
         QTT_TRY(qr_cert_spec(s, N, m, core, N, nullptr, 1, tr.p, m, norm_dev, dscale, sc.p + 16, sflag));
         ok = 1;
       } else {
-        int bad = 0;
-        QTT_TRY(spec_bad(&bad));
-        if (bad) return kOk;
+        if (spec_k) {
+          int bad = 0;
+          QTT_TRY(spec_bad(&bad));
+          if (bad) return kOk;
+        }
         QrInfo qi;
         double hd = 0.0;
         QTT_TRY(qr(s, N, m, core, N, nullptr, 1, tr.p, m, nullptr, false, &qi));
@@ -354,10 +359,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
           QTT_TRY(fetch(s, flags, &ok));
         }
       }
-      if (!ok && sflag) {
-        *spec_failed = 1;
-        return kOk;
-      }
+      if (!ok) spec_lr = false;
       if (ok) {
         newk = m;
         QTT_TRY(dgemm(s, 0, 0, mc, m, N, 1.0, next, mc, core, N, 0.0, tc.p, mc));
