@@ -297,7 +297,7 @@ int qtt_svd(int64_t m, int64_t n, const double* a, int64_t lda, double* s, doubl
   if (M >= N) {
     QTT_CUDA(cudaMallocAsync(&Q, sizeof(double) * (int64_t)M * k, st));
     QTT_CUDA(cudaMallocAsync(&tmp, sizeof(double) * (int64_t)M * k, st));
-    QTT_TRY(qr(st, M, N, a, lda, Q, M, R, k));
+    QTT_TRY(qr(st, M, N, a, lda, Q, M, R, k, nullptr, true));  // SVD inputs are ill-conditioned by design
     QTT_TRY(transpose(st, k, k, R, k, X, k));
     QTT_TRY(jacobi(st, k, k, X, k, W, k));
     QTT_TRY(sort_chop(st, k, k, X, k, s, perm, nullptr, 0.0, k, 0, rank));
@@ -308,7 +308,7 @@ int qtt_svd(int64_t m, int64_t n, const double* a, int64_t lda, double* s, doubl
   } else {
     QTT_CUDA(cudaMallocAsync(&tmp, sizeof(double) * (int64_t)M * N, st));
     QTT_TRY(transpose(st, M, N, a, lda, tmp, N));
-    QTT_TRY(qr(st, N, M, tmp, N, nullptr, 1, R, k));
+    QTT_TRY(qr(st, N, M, tmp, N, nullptr, 1, R, k, nullptr, true));
     QTT_TRY(copy_matrix(st, k, k, R, k, X, k));
     QTT_TRY(jacobi(st, k, k, X, k, W, k));
     QTT_TRY(sort_chop(st, k, k, X, k, s, perm, nullptr, 0.0, k, 0, rank));

@@ -67,7 +67,7 @@ constexpr int kSpecMax = 128;  // largest factor dimension handled without a hos
 // disables the early stop.
 int qr_sweep_right(cudaStream_t s, int from, std::vector<int64_t>& r, const std::vector<int64_t>& n,
                    const std::vector<int64_t>& off, double* work, double* tq, double* tr,
-                   double* tc, int zone, int* centre, int* sflag = nullptr) {
+                   double* tc, int zone, int* centre, int* sflag = nullptr, bool careful = false) {
   PhaseTimer pt(s);
   *centre = 0;
   for (int k = from; k >= 1; --k) {
@@ -93,7 +93,7 @@ int qr_sweep_right(cudaStream_t s, int from, std::vector<int64_t>& r, const std:
         QTT_TRY(fetch(s, sflag, &bad));
         if (bad) return kOk;
       }
-      QTT_TRY(qr(s, rows, cols, work + off[k], rows, tq, rows, tr, kk, sflag));
+      QTT_TRY(qr(s, rows, cols, work + off[k], rows, tq, rows, tr, kk, sflag, careful));
       pt.lap("rl-qr", k, rows, cols, prev);
       QTT_CUDA(cudaMemcpyAsync(work + off[k], tq, sizeof(double) * rows * (int64_t)kk,
                                cudaMemcpyDeviceToDevice, s));
@@ -186,7 +186,10 @@ int qr_cert_spec(cudaStream_t s, int m, int n, const double* A, int64_t lda, dou
 // *spec_failed = 1, the slots hold garbage and the caller reruns the
 // rounding from its input with spec_failed == nullptr.
 int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vector<int64_t>& n,
-                const std::vector<int64_t>& off, double* work, double eps, int* spec_failed) {
+                const std::vector<int64_t>& off, double* work, double eps, int* spec_failed,
+                bool careful) {
+  // careful: skip the CholeskyQR2 attempt for small factors (a thread whose
+  // recent roundings met rank-deficient cores goes straight to Householder)
   if (spec_failed) *spec_failed = 0;
   if (d == 1) return kOk;
   int64_t maxcore = 1;
@@ -222,7 +225,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
   pt.lap("reduce-left", zone, 0, 0, 0);
   static const bool no_zone = getenv("QTT_ROUND_NO_ZONE") != nullptr;
   if (no_zone) zone = -1;
-  QTT_TRY(qr_sweep_right(s, d - 1, r, n, off, work, tq.p, tr.p, tc.p, zone, &centre, sflag));
+  QTT_TRY(qr_sweep_right(s, d - 1, r, n, off, work, tq.p, tr.p, tc.p, zone, &centre, sflag, careful));
   QTT_TRY(frob_norm(s, r[centre] * n[centre] * r[centre + 1], work + off[centre], norm_dev));
   const double dscale = eps / std::sqrt((double)std::max(d - 1, 1));
   pt.lap("rl-sweep", centre, 0, 0, 0);
@@ -263,7 +266,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
       if (!ok) {
         QrInfo qi;
         double hd = 0.0;
-        QTT_TRY(qr(s, p, rc, work + off[centre], p, nullptr, 1, tr.p, rc, nullptr, false, &qi));
+        QTT_TRY(qr(s, p, rc, work + off[centre], p, nullptr, 1, tr.p, rc, nullptr, careful, &qi));
         if (qi.valid) QTT_TRY(host_delta(&hd));
         if (qi.valid && host_certificate(qi, rc, hd)) {
           ok = 1;
@@ -277,7 +280,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
     if (!ok) {
       spec_lr = false;
       int c2 = 0;
-      QTT_TRY(qr_sweep_right(s, centre, r, n, off, work, tq.p, tr.p, tc.p, -1, &c2));
+      QTT_TRY(qr_sweep_right(s, centre, r, n, off, work, tq.p, tr.p, tc.p, -1, &c2, nullptr, careful));
       QTT_TRY(frob_norm(s, r[0] * n[0] * r[1], work + off[0], norm_dev));
       norm_host = -1.0;
       centre = 0;
@@ -309,7 +312,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
         }
         QrInfo qi;
         double hd = 0.0;
-        QTT_TRY(qr(s, m, N, lc.p, m, tq.p, m, tr.p, N, nullptr, false, &qi));
+        QTT_TRY(qr(s, m, N, lc.p, m, tq.p, m, tr.p, N, nullptr, careful, &qi));
         pt.lap("lr-qr", k, m, N, mc);
         if (qi.valid) QTT_TRY(host_delta(&hd));
         if (qi.valid && host_certificate(qi, N, hd)) {
@@ -350,7 +353,7 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
         }
         QrInfo qi;
         double hd = 0.0;
-        QTT_TRY(qr(s, N, m, core, N, nullptr, 1, tr.p, m, nullptr, false, &qi));
+        QTT_TRY(qr(s, N, m, core, N, nullptr, 1, tr.p, m, nullptr, careful, &qi));
         if (qi.valid) QTT_TRY(host_delta(&hd));
         if (qi.valid && host_certificate(qi, m, hd)) {
           ok = 1;
@@ -399,29 +402,30 @@ int round_tt(const qtt_layout* in, const double* in_data, double eps, qtt_layout
   DevBuf work;
   QTT_TRY(work.alloc(s, total));
   QTT_CUDA(cudaMemcpyAsync(work.p, in_data, sizeof(double) * total, cudaMemcpyDeviceToDevice, s));
-  // Speculate "no bond truncates and every small factor is well conditioned"
-  // (true for full-rank products such as BASELINE configs 2 and 3); after two
-  // failed speculations in a row this thread rounds the next eight calls on
-  // the examined path directly (assembly / solver roundings truncate at
-  // almost every bond).
+  // Speculate "every small factor is well conditioned" (true for products of
+  // random / full-rank TTs such as BASELINE configs 2 and 3).
   static const bool spec_on = getenv("QTT_ROUND_NO_SPEC") == nullptr;
-  thread_local int streak = 0, cooldown = 0;
-  bool done = false;
+  thread_local int cooldown = 0;
+  bool done = false, careful = false;
   if (spec_on && cooldown == 0) {
     int failed = 0;
-    QTT_TRY(round_slots(s, d, r, n, off, work.p, eps, &failed));
+    QTT_TRY(round_slots(s, d, r, n, off, work.p, eps, &failed, false));
     if (!failed) {
-      streak = 0;
       done = true;
     } else {
-      if (++streak >= 2) cooldown = 8, streak = 0;
+      // rank-deficient or ill-conditioned small cores (sums of TT terms in
+      // assembly / coupling / the solver): this thread's next 16 roundings
+      // go straight to the Householder path
+      cooldown = 16;
+      careful = true;
       for (int k = 0; k <= d; ++k) r[k] = in->ranks[k];
       QTT_CUDA(cudaMemcpyAsync(work.p, in_data, sizeof(double) * total, cudaMemcpyDeviceToDevice, s));
     }
   } else if (cooldown > 0) {
     --cooldown;
+    careful = true;
   }
-  if (!done) QTT_TRY(round_slots(s, d, r, n, off, work.p, eps, nullptr));
+  if (!done) QTT_TRY(round_slots(s, d, r, n, off, work.p, eps, nullptr, careful));
   *out = *in;
   for (int k = 0; k <= d; ++k) out->ranks[k] = r[k];
   pack_offsets(out);
