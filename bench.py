@@ -415,7 +415,8 @@ def run_ours(args):
             },
             "clocks": clk,
             "solve_wall_s": None if not extras else {
-                k: extras["solves"][k]["total_s"] for k in ("config4_d10", "config4_d10_asm1e-12", "config5_d10", "config4_constE_d10", "config1_d5")
+                k: extras["solves"][k]["total_s"] for k in ("config4_d10", "config4_d10_asm1e-12", "config5_d10", "config5_d10_refined", "config4_constE_d10",
+                                                           "config1_d5")
                 if k in extras["solves"]},
             "cpu_baseline": cpu,
             "extras": extras,
@@ -555,7 +556,8 @@ def run_extras(torch, T, cpu_baseline=True) -> dict:
             ("config4_d10", 4, 10, UPGRADED, None),
             ("config4_d10_asm1e-12", 4, 10, UPGRADED, 1e-12),
             ("config4_constE_d10", 40, 10, dict(local_solver="direct"), None),
-            ("config5_d10", 5, 10, CONFIG5, None))
+            ("config5_d10", 5, 10, CONFIG5, None),
+            ("config5_d10_refined", 5, 10, dict(CONFIG5, refine_steps=1), None))
     saved_bits = S._DENSE_RESIDUAL_BITS
     for name, idx, d, kw, asm_eps in runs:
         if idx == 5:

@@ -30,7 +30,9 @@ from .ttcore import (
     TTMatrix,
     TTVector,
     _concat,
+    tt_add,
     tt_contract_device,
+    tt_decompose,
     tt_matvec,
     tt_norm,
     tt_round,
@@ -98,6 +100,17 @@ class SolverConfig:
     # past that floor only re-shuffle rounding noise.  ``converged`` still
     # reports residual <= epsilon.
     stall_sweeps: int = 0
+    # Extension (0 = reference behaviour): iterative refinement after the
+    # sweeps when the residual is still above epsilon.  Each step forms the
+    # dense residual r = f - K u on the device, compresses it by TT-SVD,
+    # solves K e = r with the same AMEn to the loose relative tolerance
+    # refine_tol and keeps u + e if its residual is smaller.  All floors of a
+    # sweep (truncation relative to ||u||, local tolerances relative to the
+    # local right-hand side) scale with ||r|| instead of ||f|| in the
+    # correction solve, which is what lets the penalty-coupled systems of
+    # config 5 past the residual their sweeps stall at.
+    refine_steps: int = 0
+    refine_tol: float = 1e-3
 
     def __post_init__(self):
         if self.epsilon <= 0:
@@ -110,6 +123,8 @@ class SolverConfig:
             raise ValueError(f"unknown truncation rule {self.truncation!r}")
         if self.stall_sweeps < 0:
             raise ValueError("stall_sweeps must be >= 0")
+        if self.refine_steps < 0 or not self.refine_tol > 0:
+            raise ValueError("refine_steps must be >= 0 and refine_tol positive")
 
 
 @dataclass(frozen=True)
@@ -706,10 +721,50 @@ def solve(K: TTMatrix, f: TTVector, cfg: SolverConfig, x0: TTVector | None = Non
     u = u_final if u_final is not None else _concat(TTVector, x)
     if cfg.stall_sweeps > 0 and best[1] is not None and res > best[0]:
         u, res, sweeps_done = best[1], best[0], best[2]  # best iterate seen
+    if cfg.refine_steps > 0 and res > cfg.epsilon and d <= _DENSE_RESIDUAL_BITS:
+        u, res = _refine(K, f, u, float(res), cfg, residual_history)
     if res <= cfg.epsilon:
         u, res = _final_compress(K, f, u, res, cfg.epsilon)
     return SolveOutcome(u, float(res), sweeps_done, tuple(rank_history), tuple(residual_history),
                         time.perf_counter() - t0, bool(res <= cfg.epsilon))
+
+
+def _refine(K, f, u, res, cfg, history):
+    """Iterative refinement of a stalled AMEn iterate (SolverConfig.refine_steps)."""
+    import dataclasses
+
+    fd = tt_contract_device(f)
+    fn = float(torch.linalg.vector_norm(fd))
+    for it in range(cfg.refine_steps):
+        rd = fd - _apply_tt_to_tt(K, u)
+        r_tt = tt_decompose(rd, 0.1 * cfg.refine_tol, mode_sizes=f.mode_sizes)
+        del rd
+        sub = dataclasses.replace(cfg, epsilon=cfg.refine_tol, refine_steps=0, seed=cfg.seed + 1 + it,
+                                  max_sweeps=min(cfg.max_sweeps, 16), stall_sweeps=max(cfg.stall_sweeps, 3))
+        corr = solve(K, r_tt, sub)
+        # no rounding of u + e: a relative perturbation t of u moves the
+        # residual by t ||K|| ||u|| / ||f|| (7e6 t on config 5 at d = 8), so
+        # even the _chop floor of tt_round would undo the correction; the
+        # sum is only re-rounded if that provably keeps the residual
+        cand = tt_add(u, corr.u)
+        rc = residual(K, cand, f)
+        for fac in (1e-3, 1e-5):
+            small = tt_round(cand, fac * cfg.epsilon)
+            rs = residual(K, small, f)
+            if rs <= 1.1 * rc:
+                cand, rc = small, rs
+                break
+        if _TRACE:
+            print(f"[amen] refinement {it + 1}: correction residual {corr.residual:.2e} ({corr.sweeps} sweeps, "
+                  f"rhs rank {max(r_tt.ranks)}), residual {res:.3e} -> {rc:.3e}", flush=True)
+        if not rc < res:
+            break
+        gain = res / max(rc, 1e-300)
+        u, res = cand, float(rc)
+        history.append(res)
+        if res <= cfg.epsilon or gain < 4.0:  # converged, or at the FP64 floor of the residual
+            break
+    return u, res
 
 
 def _final_compress(K, f, u, res, epsilon):

@@ -288,15 +288,24 @@ def test_config4_solve_against_conforming(config4_system):
 
 
 def test_config5_d8_against_conforming():
-    """L-shape (3 patches, penalty coupling) at 2^8 x 2^8 per patch: AMEn with
-    the stall rule reaches the FP64 residual floor (||K|| ||u|| / ||f|| ~ 7e6)
-    and its solution agrees with the conforming splu solution."""
+    """L-shape (3 patches, penalty coupling) at 2^8 x 2^8 per patch.  The
+    AMEn sweeps stall at a residual of ~4e-7 (every floor of a sweep is
+    relative to ||u||, and ||K|| ||u|| / ||f|| ~ 7e6 here); one step of
+    iterative refinement (SolverConfig.refine_steps, the correction solve's
+    floors are relative to the residual) brings the dense-operator residual
+    below eps.  The forward error is measured against the merged-node
+    conforming FEM, from which the EXACT solution of the penalty-coupled QTT
+    system is itself ~5e-9 away (profiles/r02_config5_d8_cg_exact.log), and a
+    residual-<=-eps iterate of the reference is ~1.5e-8 away from its truth
+    (SURVEY §8(d)): gate 2.5e-8."""
     from paper_2501_07778_b200 import solver as S
     from paper_2501_07778_b200.configs import build_system
 
     gsys, eps = build_system(5, 8)
     res = S.solve(gsys.K, gsys.f, S.SolverConfig(epsilon=eps, seed=0, max_sweeps=25, stall_sweeps=4,
-                                                 **CONFIG5))
+                                                 refine_steps=2, **CONFIG5))
+    assert max(gsys.K.ranks) == 85
+    assert res.converged and res.residual <= eps, (res.residual, res.sweeps)
     uc, c = _conforming(5, 8)
     err = rel_diff(res.u, uc)
     assert err <= CONFIG5_GATE, (err, res.residual, res.sweeps)
@@ -304,4 +313,4 @@ def test_config5_d8_against_conforming():
 
 CONFIG5 = dict(local_solver="auto", truncation="residual", enrichment_rank=24, local_rtol_factor=1e-3,
                trunc_factor=0.05)
-CONFIG5_GATE = 1e-8
+CONFIG5_GATE = 2.5e-8
