@@ -43,6 +43,197 @@ __global__ void __launch_bounds__(256) lu_diag_kernel(int kb, double* __restrict
   blk_store(y, linv, LB, LB);
 }
 
+
+// ------------------------------------------------------- diagonal block, v2
+// Same contract as lu_diag_kernel, organised for latency like the small
+// Cholesky kernel (cholqr.cu): 2 x 2 blocks of 32; each 32 x 32 leaf is
+// factored by ONE warp out of registers (lane l owns column l, the
+// multipliers of a pivot step travel through a double-buffered shared line:
+// one __syncwarp per pivot instead of a block barrier), its two triangular
+// inverses by two warps side by side, and panels, Schur update and the
+// off-diagonal inverse blocks are 32^3 block products over the 8 warps.
+constexpr int kL2 = 32, kL2Ld = kBlk + 1;
+constexpr int kLu2Smem = (3 * kBlk * kL2Ld + kL2 * (kL2 + 1) + 2 * kL2 + 8) * (int)sizeof(double);
+
+// LU without pivoting of the 32 x 32 leaf at (k0, k0) of M, in place; one warp.
+__device__ __forceinline__ void lu2_leaf(double* M, double* cb, int k0, int* bad) {
+  const int l = threadIdx.x & 31;
+  double col[kL2];
+#pragma unroll
+  for (int i = 0; i < kL2; ++i) col[i] = M[(k0 + i) * kL2Ld + k0 + l];
+#pragma unroll
+  for (int j = 0; j < kL2; ++j) {
+    const double p = __shfl_sync(0xffffffffu, col[j], j);
+    if (l == 0 && !(fabs(p) > 0.0)) *bad = 1;
+    const double inv = rcp_nr(p);
+    double* b = cb + (j & 1) * kL2;
+    if (l == j) {
+#pragma unroll
+      for (int i = j + 1; i < kL2; ++i) {
+        col[i] *= inv;  // multipliers L[i][j]
+        b[i] = col[i];
+      }
+    }
+    __syncwarp();
+    if (l > j) {
+      const double u = col[j];  // U[j][l]
+#pragma unroll
+      for (int i = j + 1; i < kL2; ++i) col[i] = fma(-b[i], u, col[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kL2; ++i) M[(k0 + i) * kL2Ld + k0 + l] = col[i];
+}
+
+// Column l of U^{-1} (upper) of the leaf at (k0, k0): X[i][l] -> Ui[k0 + i][k0 + l].
+__device__ __forceinline__ void lu2_uinv(const double* M, double* Ui, int k0) {
+  const int l = threadIdx.x & 31;
+  double v[kL2];
+#pragma unroll
+  for (int i = 0; i < kL2; ++i) v[i] = 0.0;
+#pragma unroll
+  for (int k2 = kL2 - 1; k2 >= 0; --k2) {
+    const double dinv = rcp_nr(M[(k0 + k2) * kL2Ld + k0 + k2]);
+    const double xk = (l == k2) ? dinv : (l > k2 ? -v[k2] * dinv : 0.0);
+    v[k2] = xk;
+    const double* ucol = M + (size_t)k0 * kL2Ld + k0 + k2;
+#pragma unroll
+    for (int i = 0; i < k2; ++i) v[i] = fma(ucol[i * kL2Ld], xk, v[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < kL2; ++i) Ui[(k0 + i) * kL2Ld + k0 + l] = v[i];  // zero below the diagonal
+}
+
+// Column l of L^{-1} (unit lower) of the leaf at (k0, k0) -> Li[k0 + i][k0 + l].
+__device__ __forceinline__ void lu2_linv(const double* M, double* Li, int k0) {
+  const int l = threadIdx.x & 31;
+  double v[kL2];
+#pragma unroll
+  for (int i = 0; i < kL2; ++i) v[i] = 0.0;
+#pragma unroll
+  for (int k2 = 0; k2 < kL2; ++k2) {
+    const double yk = (l == k2) ? 1.0 : (l < k2 ? -v[k2] : 0.0);
+    v[k2] = yk;
+    const double* lcol = M + (size_t)k0 * kL2Ld + k0 + k2;
+#pragma unroll
+    for (int i = k2 + 1; i < kL2; ++i) v[i] = fma(lcol[i * kL2Ld], yk, v[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < kL2; ++i) Li[(k0 + i) * kL2Ld + k0 + l] = v[i];  // zero above the diagonal
+}
+
+// out[q] = sum_k A[(i0+q)][k] * B[k][c] over k in [0, 32): A rows warp-uniform
+// (broadcast reads), B row-contiguous in c.  A, B point at block origins,
+// row stride kL2Ld.
+__device__ __forceinline__ void lu2_mm(const double* A, const double* B, int i0, int c, double (&out)[4]) {
+  out[0] = out[1] = out[2] = out[3] = 0.0;
+  const double* a = A + (size_t)i0 * kL2Ld;
+#pragma unroll 8
+  for (int k2 = 0; k2 < kL2; ++k2) {
+    const double bv = B[k2 * kL2Ld + c];
+    out[0] = fma(a[k2], bv, out[0]);
+    out[1] = fma(a[kL2Ld + k2], bv, out[1]);
+    out[2] = fma(a[2 * kL2Ld + k2], bv, out[2]);
+    out[3] = fma(a[3 * kL2Ld + k2], bv, out[3]);
+  }
+}
+
+__global__ void __launch_bounds__(256) lu_diag2_kernel(int kb, double* __restrict__ A, int64_t lda,
+                                                       double* __restrict__ linv,
+                                                       double* __restrict__ uinv,
+                                                       int* __restrict__ bad) {
+  extern __shared__ double lu2_sm[];
+  double* M = lu2_sm;                   // 64 x 65: A, then L \ U
+  double* Li = M + kBlk * kL2Ld;        // L^{-1}
+  double* Ui = Li + kBlk * kL2Ld;       // U^{-1}
+  double* T = Ui + kBlk * kL2Ld;        // 32 x 33
+  double* cb = T + kL2 * (kL2 + 1);     // 2 x 32 multiplier line
+  __shared__ int bad_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) bad_s = 0;
+  for (int idx = tid; idx < kBlk * kBlk; idx += 256) {
+    const int i = idx % kBlk, j = idx / kBlk;
+    M[i * kL2Ld + j] = (i < kb && j < kb) ? A[i + (int64_t)j * lda] : (i == j ? 1.0 : 0.0);
+    Li[i * kL2Ld + j] = 0.0;
+    Ui[i * kL2Ld + j] = 0.0;
+  }
+  __syncthreads();
+  const int i0 = warp * 4, c = lane;
+  double o1[4], o2[4];
+  double* M12 = M + kL2;
+  double* M21 = M + kL2 * kL2Ld;
+  double* M22 = M + kL2 * kL2Ld + kL2;
+  // ---- leaf (0, 0) and its inverses
+  if (warp == 0) lu2_leaf(M, cb, 0, &bad_s);
+  __syncthreads();
+  if (warp == 0) lu2_uinv(M, Ui, 0);
+  if (warp == 1) lu2_linv(M, Li, 0);
+  __syncthreads();
+  // ---- panels: U12 = L11^{-1} A12, L21 = A21 U11^{-1}
+  lu2_mm(Li, M12, i0, c, o1);
+  lu2_mm(M21, Ui, i0, c, o2);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    M12[(i0 + q) * kL2Ld + c] = o1[q];
+    M21[(i0 + q) * kL2Ld + c] = o2[q];
+  }
+  __syncthreads();
+  // ---- Schur complement and leaf (1, 1)
+  lu2_mm(M21, M12, i0, c, o1);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) M22[(i0 + q) * kL2Ld + c] -= o1[q];
+  __syncthreads();
+  if (warp == 0) lu2_leaf(M, cb, kL2, &bad_s);
+  __syncthreads();
+  if (warp == 0) lu2_uinv(M, Ui, kL2);
+  if (warp == 1) lu2_linv(M, Li, kL2);
+  __syncthreads();
+  // ---- off-diagonal inverse blocks: Ui12 = -Ui11 (U12 Ui22), Li21 = -Li22 (L21 Li11)
+  lu2_mm(M12, Ui + kL2 * kL2Ld + kL2, i0, c, o1);  // U12 Ui22
+#pragma unroll
+  for (int q = 0; q < 4; ++q) T[(i0 + q) * (kL2 + 1) + c] = o1[q];
+  __syncthreads();
+  {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const double* a = Ui + (size_t)i0 * kL2Ld;
+#pragma unroll 8
+    for (int k2 = 0; k2 < kL2; ++k2) {
+      const double tv = T[k2 * (kL2 + 1) + c];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(a[q * kL2Ld + k2], tv, acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Ui[(i0 + q) * kL2Ld + kL2 + c] = -acc[q];
+  }
+  __syncthreads();
+  lu2_mm(M21, Li, i0, c, o1);  // L21 Li11
+#pragma unroll
+  for (int q = 0; q < 4; ++q) T[(i0 + q) * (kL2 + 1) + c] = o1[q];
+  __syncthreads();
+  {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const double* a = Li + (size_t)(kL2 + i0) * kL2Ld + kL2;  // Li22 rows
+#pragma unroll 8
+    for (int k2 = 0; k2 < kL2; ++k2) {
+      const double tv = T[k2 * (kL2 + 1) + c];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = fma(a[q * kL2Ld + k2], tv, acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Li[(kL2 + i0 + q) * kL2Ld + c] = -acc[q];
+  }
+  __syncthreads();
+  // ---- write back: A <- L \ U (active part), linv / uinv full 64 x 64 (ld 64)
+  for (int idx = tid; idx < kBlk * kBlk; idx += 256) {
+    const int i = idx % kBlk, j = idx / kBlk;
+    if (i < kb && j < kb) A[i + (int64_t)j * lda] = M[i * kL2Ld + j];
+    linv[i + j * kBlk] = Li[i * kL2Ld + j];
+    uinv[i + j * kBlk] = Ui[i * kL2Ld + j];
+  }
+  if (tid == 0 && bad_s) *bad = 1;
+}
+
 __global__ void residual_norms_kernel(int n, const double* __restrict__ r,
                                       const double* __restrict__ b, double* out) {
   __shared__ double s1[32], s2[32];
@@ -73,6 +264,16 @@ __global__ void axpy_kernel(int n, const double* __restrict__ d, double* __restr
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] += d[i];
 }
 
+int launch_lu_diag(cudaStream_t st, int kb, double* A, int64_t lda, double* linv, double* uinv, int* bad) {
+  static const bool v1 = getenv("QTT_LU_DIAG_V1") != nullptr;
+  if (v1)
+    lu_diag_kernel<<<1, 256, kLuSmem, st>>>(kb, A, lda, linv, uinv, bad);
+  else
+    lu_diag2_kernel<<<1, 256, kLu2Smem, st>>>(kb, A, lda, linv, uinv, bad);
+  QTT_CHECK_LAUNCH();
+  return kOk;
+}
+
 }  // namespace
 
 // Solve M x = b (M: N x N column-major, ldm).  Returns kOk; *fallback
@@ -83,6 +284,7 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
   static DeviceFlag configured;
   if (!configured.test()) {
     QTT_CUDA(cudaFuncSetAttribute(lu_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLuSmem));
+    QTT_CUDA(cudaFuncSetAttribute(lu_diag2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kLu2Smem));
     configured.set();
   }
   const int64_t ld = N;
@@ -118,8 +320,7 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
   double *Lp, *Up;
   QTT_CUDA(cudaMallocAsync(&Lp, sizeof(double) * ld * LB, s));
   QTT_CUDA(cudaMallocAsync(&Up, sizeof(double) * (int64_t)LB * (N + 1), s));
-  lu_diag_kernel<<<1, 256, kLuSmem, s>>>(std::min(LB, N), A, ld, linv, uinv, bad);
-  QTT_CHECK_LAUNCH();
+  QTT_TRY(launch_lu_diag(s, std::min(LB, N), A, ld, linv, uinv, bad));
   // Two-level blocking for large N: block pairs (a, b) share ONE trailing
   // update with K = 128 (a's update of the rows below b is deferred to b),
   // which runs the Schur complement GEMM at a higher DMMA efficiency than
@@ -160,9 +361,8 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
         QTT_TRY(dgemm(s, 0, 0, m2, kb1, KK, -1.0, Lab, ld, Uab, ld, 1.0, A22n, ld));
         QTT_CUDA(cudaEventRecord(ev_col, s));
         QTT_CUDA(cudaStreamWaitEvent(sb, ev_col, 0));
-        lu_diag_kernel<<<1, 256, kLuSmem, sb>>>(kb1, A22n, ld, linv + (int64_t)(blk + 1) * LB * LB,
-                                                uinv + (int64_t)(blk + 1) * LB * LB, bad);
-        QTT_CHECK_LAUNCH();
+        QTT_TRY(launch_lu_diag(sb, kb1, A22n, ld, linv + (int64_t)(blk + 1) * LB * LB,
+                               uinv + (int64_t)(blk + 1) * LB * LB, bad));
         QTT_CUDA(cudaEventRecord(ev_diag, sb));
         if (rest > 0)
           QTT_TRY(dgemm(s, 0, 0, m2, rest, KK, -1.0, Lab, ld, Uab + (int64_t)kb1 * ld, ld, 1.0,
@@ -171,9 +371,8 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
         QTT_TRY(dgemm(s, 0, 0, m2, kb1, kb, -1.0, Lp, m2, Up, kb, 1.0, A22n, ld));
         QTT_CUDA(cudaEventRecord(ev_col, s));
         QTT_CUDA(cudaStreamWaitEvent(sb, ev_col, 0));
-        lu_diag_kernel<<<1, 256, kLuSmem, sb>>>(kb1, A22n, ld, linv + (int64_t)(blk + 1) * LB * LB,
-                                                uinv + (int64_t)(blk + 1) * LB * LB, bad);
-        QTT_CHECK_LAUNCH();
+        QTT_TRY(launch_lu_diag(sb, kb1, A22n, ld, linv + (int64_t)(blk + 1) * LB * LB,
+                               uinv + (int64_t)(blk + 1) * LB * LB, bad));
         QTT_CUDA(cudaEventRecord(ev_diag, sb));
         if (rest > 0) {
           // pair_a: only the partner's rows (needed for its U12); the rows
@@ -263,8 +462,7 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
       const int kb = std::min(LB, N - kb0);
       // invert the diagonal block of R through the LU kernel (L = I)
       QTT_TRY(copy_matrix(s, kb, kb, R + kb0 + (int64_t)kb0 * ld, ld, tmp, LB));
-      lu_diag_kernel<<<1, 256, kLuSmem, s>>>(kb, tmp, LB, linv, uinv, bad);
-      QTT_CHECK_LAUNCH();
+      QTT_TRY(launch_lu_diag(s, kb, tmp, LB, linv, uinv, bad));
       QTT_TRY(dgemm(s, 0, 0, kb, 1, kb, 1.0, uinv, LB, y + kb0, N, 0.0, x + kb0, N));
       if (kb0 > 0)
         QTT_TRY(dgemm(s, 0, 0, kb0, 1, kb, -1.0, R + (int64_t)kb0 * ld, ld, x + kb0, N, 1.0, y, N));

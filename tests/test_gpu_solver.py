@@ -236,3 +236,18 @@ def test_apply_tt_to_tt_matches_dense_chain(d, rk, ru):
     ref = S.apply_tt_matrix(K, T.tt_contract_device(u))
     assert y.shape == ref.shape
     assert float(torch.linalg.vector_norm(y - ref) / torch.linalg.vector_norm(ref)) < 1e-13
+
+
+def test_cli_run_and_snapshot(tmp_path):
+    """bench_cli: one config-1 row at d = 4 and a TT snapshot round trip."""
+    from paper_2501_07778_b200 import cli, ttio
+    from paper_2501_07778_b200 import ttcore as T
+
+    out, snap = tmp_path / "row.csv", tmp_path / "u.qtt"
+    assert cli.main(["run", "--case", "config1", "--d", "4", "--eps", "1e-8", "--out", str(out),
+                     "--save-u", str(snap)]) == 0
+    (row,) = ttio.read_csv(str(out))
+    assert row.case == "config1" and row.d == 4 and row.dofs == 2 * 4**4 and row.converged
+    assert row.l2_error < 1e-8  # against tests/golden/conforming_c1_d4.npz
+    u = ttio.load_tt(str(snap))
+    assert max(u.ranks) == row.Rd and T.rank_profile(u).param_count == row.Nd
