@@ -316,8 +316,11 @@ _LOCAL_HOOK = None  # diagnostics: called with (phi_l, a_p, phi_r, rhs, x_cur, s
 _ITERATIVE_MIN_DIM = 8192
 _GMRES_RESTART = 40
 _GMRES_MAXIT = 400
-# beyond this dimension a dense fallback would not fit comfortably
-_DENSE_FALLBACK_MAX = 60000
+# beyond this dimension a dense fallback costs seconds ((2/3) N^3 flops: 0.4 s
+# at 24,000, 6 s at 60,000, which is what a stalling config-5 sweep used to
+# spend on local systems GMRES cannot resolve below the FP64 floor); the
+# warm-started GMRES iterate, never worse than the current core, is kept
+_DENSE_FALLBACK_MAX = 24000
 
 
 def _local_matvec(phi_l, a_p, phi_r, x):
