@@ -384,7 +384,14 @@ def run_ours(args):
                 "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json has no FP64 entry)",
                 "unit": "TFLOP/s",
                 "frac": round(achieved / fp64_peak, 4) if fp64_peak else None,
-                "traffic": None,
+                # dram__bytes_read.sum + dram__bytes_write.sum of the largest GEMM launch of the
+                # step (ncu --set full, profiles/r02_kernel_evidence.txt): the 2048 x 4096 x 2048
+                # carry product of the (16,128) pair, 34.4 GFLOP in 1.03 ms (33 TF/s) -- 262.5 MB read +
+                # 53.6 MB written against 167.8 MB algorithmic (A, B once + C once); `achieved` is the
+                # aggregate over ALL GEMM launches of the serial step, so this is per top launch
+                "traffic": 316.1e6,
+                "traffic_launch": {"shape": "2048x4096x2048", "gflop": 34.36, "ms": 1.033, "tflops": 33.3,
+                                   "algorithmic_bytes": 167.8e6},
                 "gemm_launches_per_step": int(glaunch),
                 "gemm_share_of_step": round(gms / serial_ms, 4),
                 "step_nominal_tflops_frac": round(value / 1e3 / fp64_peak, 4),

@@ -246,6 +246,35 @@ def test_round_ranks_and_error(eps):
         assert err <= eps * (1 + 1e-8) + 1e-13
 
 
+@pytest.mark.parametrize("where", ["middle", "late", "none"])
+def test_round_speculation_recovers(where):
+    """Speculative (sync-free) rounding of a rank-64 TT: full-rank head, then
+    an exactly rank-deficient bond in the middle / near the end of the sweep.
+    The sticky device flag must send the rounding back to the examined path
+    and the result must match the oracle's ranks and values; repeated calls
+    (speculation cool-down of the calling thread) give the same answer."""
+    T = _T()
+    d, r = 14, 64
+    rng = np.random.default_rng({"middle": 11, "late": 12, "none": 13}[where])
+    rk = [1] + [min(r, 2**k, 2 ** (d - k)) for k in range(1, d)] + [1]
+    cores = [rng.standard_normal((rk[k], 2, rk[k + 1])) / np.sqrt(rk[k]) for k in range(d)]
+    bond = {"middle": 7, "late": 9, "none": None}[where]
+    if bond is not None:  # core bond-1 factors through rank 20 (< 64)
+        a, n, b = cores[bond - 1].shape
+        cores[bond - 1] = (rng.standard_normal((a * n, 20)) @ rng.standard_normal((20, b))).reshape(a, n, b) / 20
+    ref = O.round_tt(cores, 1e-10)
+    want = O.ranks(ref)
+    if bond is not None:
+        assert want[bond] == 20
+    t = T.TTVector(cores)
+    full = O.full(cores)
+    for rep in range(3):
+        got = T.tt_round(t, 1e-10)
+        assert got.ranks == want, (rep, got.ranks, want)
+        err = np.linalg.norm(dense_of(got) - full) / np.linalg.norm(full)
+        assert err <= 1e-10 * (1 + 1e-8) + 1e-13
+
+
 def test_round_matrix():
     T = _T()
     rng = np.random.default_rng(5)
