@@ -468,11 +468,12 @@ constexpr int kC2Smem =
 
 // Factor + invert the 32 x 32 diagonal leaf at (k0, k0); executed by one warp.
 // R_kk -> upper triangle of M, X_kk -> xdk (32 x 33, zero below the diagonal).
+template <int LD, bool INV>
 __device__ __forceinline__ void c2_leaf(double* M, double* xdk, double* rowbuf, int k0, int* bad) {
   const int l = threadIdx.x & 31;
   double col[kC2], dinv[kC2];
 #pragma unroll
-  for (int i = 0; i < kC2; ++i) col[i] = M[(k0 + i) * kC2Ld + k0 + l];
+  for (int i = 0; i < kC2; ++i) col[i] = M[(k0 + i) * LD + k0 + l];
 #pragma unroll
   for (int j = 0; j < kC2; ++j) {
     const double p = __shfl_sync(0xffffffffu, col[j], j);
@@ -489,22 +490,24 @@ __device__ __forceinline__ void c2_leaf(double* M, double* xdk, double* rowbuf, 
   }
 #pragma unroll
   for (int i = 0; i < kC2; ++i)
-    if (i <= l) M[(k0 + i) * kC2Ld + k0 + l] = col[i];
+    if (i <= l) M[(k0 + i) * LD + k0 + l] = col[i];
   __syncwarp();
-  // column l of X = R^{-1}: v[i] accumulates sum_k R[i][k] x[k] until it becomes x[i]
-  double v[kC2];
+  if constexpr (INV) {
+    // column l of X = R^{-1}: v[i] accumulates sum_k R[i][k] x[k] until it becomes x[i]
+    double v[kC2];
 #pragma unroll
-  for (int i = 0; i < kC2; ++i) v[i] = 0.0;
+    for (int i = 0; i < kC2; ++i) v[i] = 0.0;
 #pragma unroll
-  for (int k2 = kC2 - 1; k2 >= 0; --k2) {
-    const double xk = (l == k2) ? dinv[k2] : (l > k2 ? -v[k2] * dinv[k2] : 0.0);
-    v[k2] = xk;
-    const double* rcol = M + (size_t)k0 * kC2Ld + k0 + k2;  // R[i][k2], i < k2 (broadcast reads)
+    for (int k2 = kC2 - 1; k2 >= 0; --k2) {
+      const double xk = (l == k2) ? dinv[k2] : (l > k2 ? -v[k2] * dinv[k2] : 0.0);
+      v[k2] = xk;
+      const double* rcol = M + (size_t)k0 * LD + k0 + k2;  // R[i][k2], i < k2 (broadcast reads)
 #pragma unroll
-    for (int i = 0; i < k2; ++i) v[i] = fma(rcol[i * kC2Ld], xk, v[i]);
+      for (int i = 0; i < k2; ++i) v[i] = fma(rcol[i * LD], xk, v[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < kC2; ++i) xdk[i * (kC2 + 1) + l] = v[i];  // zero for i > l
   }
-#pragma unroll
-  for (int i = 0; i < kC2; ++i) xdk[i * (kC2 + 1) + l] = v[i];  // zero for i > l
 }
 
 __global__ void __launch_bounds__(256) chol_inv_small2_kernel(int n, const double* __restrict__ G,
@@ -584,7 +587,7 @@ __global__ void __launch_bounds__(256) chol_inv_small2_kernel(int n, const doubl
   const int c = lane, i0 = warp * 4;  // thread tile: rows i0..i0+3 of a block, column c
   for (int kb = 0; kb < nb; ++kb) {
     const int k0 = kb * kC2;
-    if (warp == 0) c2_leaf(M, Xd + kb * kC2Xd, rowbuf, k0, &bad_s);
+    if (warp == 0) c2_leaf<kC2Ld, true>(M, Xd + kb * kC2Xd, rowbuf, k0, &bad_s);
     __syncthreads();
     C2_STAMP();
     const int nj = nb - kb - 1;
@@ -774,6 +777,8 @@ int chol_upper(cudaStream_t s, int n, double* G, int64_t ldg, double* rblk, int*
     const int rest = n - k0 - kb;
     const double* Gkk = G + k0 + (int64_t)k0 * ldg;
     double* G12 = G + k0 + (int64_t)(k0 + kb) * ldg;
+    // (a variant with single-warp 32 x 32 register leaves for the diagonal factor, as in
+    // chol_inv_small2_kernel, measured no faster here: 90.9 vs 89.1 ms serial config-2 step)
     chol_panel_kernel<<<std::max(1, (int)ceil_div(rest, CB)), 256, 0, sp>>>(
         kb, Gkk, ldg, rblk + (int64_t)k * CB * CB, G12, rest, bad);
     QTT_CHECK_LAUNCH();
