@@ -37,8 +37,17 @@ __global__ void __launch_bounds__(256) chol_panel_kernel(int kb, const double* _
   __shared__ __align__(16) double line[256];
   __shared__ double dinv[kBlk];
   double a[16];
+#ifdef QTT_PANEL_DEBUG
+  const long long t0 = clock64();
+#endif
   blk_load(a, G11, ldg, kb);
+#ifdef QTT_PANEL_DEBUG
+  const long long t1 = clock64();
+#endif
   blk_factor<true>(a, line, bad);
+#ifdef QTT_PANEL_DEBUG
+  const long long t2 = clock64();
+#endif
   if (blockIdx.x == 0) blk_store(a, rblk, kBlk, kBlk);
   const int col = blockIdx.x * kBlk + blk_col();
   if (blockIdx.x * kBlk >= rest) return;
@@ -65,6 +74,11 @@ __global__ void __launch_bounds__(256) chol_panel_kernel(int kb, const double* _
 #pragma unroll
     for (int q = qj + 1; q < 16; ++q) x[q] = fma(r[4 * q], xj, x[q]);
   }
+#ifdef QTT_PANEL_DEBUG
+  const long long t3 = clock64();
+  if (threadIdx.x == 0 && blockIdx.x == 0 && rest > 1900)
+    printf("[chol-panel] load %lld factor %lld solve %lld\n", t1 - t0, t2 - t1, t3 - t2);
+#endif
   if (act) {
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
