@@ -42,7 +42,7 @@ namespace qtt {
 namespace {
 
 constexpr int SV_PMAX = 64;                          // rows of a superstep column
-constexpr int SV_P0 = 8;                             // rows in the first (largest) pass
+constexpr int SV_P0 = 16;                            // rows in the first (largest) pass
 constexpr int SV_NT = 512;                           // threads per CTA
 constexpr int SV_NW = SV_NT / 32;
 constexpr int SV_NE = SV_PMAX * (SV_PMAX + 1) / 2;   // Gram entries (upper triangle)
