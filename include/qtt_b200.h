@@ -112,8 +112,17 @@ int qtt_scale(const qtt_layout* A, const double* a, double s, double* out,
 
 /* ------------------------------------------------------------------- (a5)
  * TT rounding, replaces ttcore.tt_round (ttcore.py:322-338):
- * right-to-left Householder QR sweep, then left-to-right truncated SVD sweep
- * with delta = eps/sqrt(d-1)*||t|| and the _chop rule (ttcore.py:175-190).
+ * right-to-left QR sweep, then left-to-right truncated SVD sweep with
+ * delta = eps/sqrt(d-1)*||t|| and the _chop rule (ttcore.py:175-190).  Same
+ * ranks and the same tensor within eps as the reference; how it gets there
+ * (DESIGN.md section 4): structurally full-rank cores are folded into
+ * identities, a bond whose triangular factor provably has no singular value
+ * at or below the _chop threshold keeps its QR factors instead of an SVD
+ * (one certificate covers every bond of the leading identity zone),
+ * otherwise one-sided Jacobi; factors of dimension <= 128 run without host
+ * synchronisation (a sticky device flag sends the call back to the examined
+ * path).  QTT_ROUND_NO_SPEC=1 / QTT_ROUND_NO_ZONE=1 switch those two off,
+ * QTT_ROUND_TRACE=1 prints per-phase device times.
  * `out` receives the final ranks/offsets; out_data needs
  * qtt_layout_size(in) doubles (ranks never increase). */
 int qtt_round(const qtt_layout* in, const double* in_data, double eps,
@@ -211,7 +220,11 @@ int qtt_gemm_structured(int32_t trans_a, int32_t trans_b, int64_t m, int64_t n,
                         int64_t k, double alpha, const double* a, int64_t lda,
                         const double* b, int64_t ldb, double beta, double* c,
                         int64_t ldc, int32_t flags, void* stream);
-/* Householder QR of a column-major m x n matrix: Q (m x k), R (k x n). */
+/* QR of a column-major m x n matrix: explicit thin Q (m x k) and upper
+ * triangular R (k x n), k = min(m, n); q may be null (R only).  Tall
+ * well-conditioned inputs take CholeskyQR2 (certified: pivot breakdown or
+ * ||Q1^T Q1 - I||_F > 1/4 falls back), everything else blocked Householder
+ * (single-CTA kernel below 64 columns, cluster panels + compact-WY above). */
 int qtt_qr(int64_t m, int64_t n, const double* a, int64_t lda, double* q,
            int64_t ldq, double* r, int64_t ldr, void* stream);
 /* Singular values (descending) and left singular vectors (u, m x min(m,n))
