@@ -491,7 +491,7 @@ def run_extras(torch, T, cpu_baseline=True) -> dict:
     * config 3: rounding (both eps) and the 2^26 TT-SVD, with the oracle port
       timed on this host in the same run;
     * solves: config 1 (reference solver path), config 4 as specified
-      (variable E, upgraded AMEn -- the reference cannot solve it,
+      (variable E, upgraded AMEn -- the reference cannot reach it at d = 10,
       profiles/r02_ref_solve_c4_d6.log), config-4 geometry with constant E on
       the reference path, config 5 (L-shape) with the stall rule, each with
       the forward error against the conforming ground truth when the fixture
@@ -582,8 +582,9 @@ def run_extras(torch, T, cpu_baseline=True) -> dict:
     solves["reference_cpu_s_survey"] = {
         "config1_d5_solve": 1.21, "config4_constE_d10_solve": 658.9, "config4_constE_d10_assembly": 11.05,
         "config4_d10_assembly": 43.0, "config4_d10_couple_dirichlet": 18.0,
-        "note": "SURVEY Appendix B (8-core Xeon); the reference solver does not converge on config 4 "
-                "as specified (variable E), profiles/r02_ref_solve_c4_d6.log"}
+        "note": "SURVEY Appendix B (8-core Xeon); on config 4 as specified (variable E) the reference's default "
+                "solver diverges and its direct-local-solve path converges at d = 6 in 246 s with full ranks "
+                "(profiles/r02_ref_solve_c4_d6.log) but cannot factor the dense local systems of d = 10"}
     if cpu_baseline:
         from oracle import amen
 

@@ -253,7 +253,7 @@ def test_config4_solve_against_conforming(config4_system):
     independent conforming FEM solved by splu (make_conforming.py).
 
     The SURVEY §8(d) gate is max(||u_ref - u_conf||, eps) + 1e-10.  The
-    reference has no converged u on this config; on the constant-E sibling its
+    reference has no converged u on this config at d = 10; on the constant-E sibling its
     own forward error at d = 10 is 1.55e-8, which is
     what a residual-<=-eps stopping rule delivers on an operator of condition
     ~1e7, so the gate used here is 2e-8 for the operator assembled accurately
