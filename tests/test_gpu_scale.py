@@ -116,6 +116,31 @@ def test_config2_large_pairs_round_error(pair):
     assert rel_diff(z, y) <= 1e-10
 
 
+@pytest.mark.parametrize("pair", [(4, 128), (8, 128)])
+def test_config2_round_properties(pair):
+    """Size-independent properties of the rounding at BASELINE size: left
+    orthonormality of every core but the last (the reference's output gauge,
+    ttcore.py:309-319), idempotence (round(round(y)) == round(y), same
+    ranks), homogeneity (round(-3 y) == -3 round(y)) and the norm carried by
+    the last core."""
+    import torch
+
+    T = _T()
+    A, x = bench.make_inputs(*pair)
+    y = T.tt_matvec(T.TTMatrix(A), T.TTVector(x))
+    z = T.tt_round(y, 1e-10)
+    cores = z.device_cores
+    for c in cores[:-1]:
+        m = c.reshape(-1, c.shape[-1])
+        g = m.T @ m
+        assert float((g - torch.eye(g.shape[0], dtype=g.dtype, device=g.device)).abs().max()) <= 1e-12
+    assert abs(float(torch.linalg.vector_norm(cores[-1])) - T.tt_norm(y)) <= 1e-11 * T.tt_norm(y)
+    zz = T.tt_round(z, 1e-10)
+    assert zz.ranks == z.ranks and rel_diff(zz, z) <= 1e-12
+    w = T.tt_round(T.tt_scale(y, -3.0), 1e-10)
+    assert w.ranks == z.ranks and rel_diff(w, T.tt_scale(z, -3.0)) <= 1e-11
+
+
 def test_config2_all_pairs_rank1_probes():
     """Size-independent property on all 9 pairs: <round(y), w> = <y, w> for
     random rank-1 w (relative to ||y|| ||w||)."""
