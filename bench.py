@@ -277,8 +277,10 @@ def run_ours(args):
 
         def e2e_job(p):
             Ah, xh = host[p]
-            z = T.tt_round(T.tt_matvec(T.TTMatrix(Ah), T.TTVector(xh)), EPS)
-            e2e_out[p] = z.numpy_cores()
+            # host=True: the rounded cores are streamed to pinned host memory while the
+            # sweep runs (qtt_round_to_host); .cores are those host arrays
+            z = T.tt_round(T.tt_matvec(T.TTMatrix(Ah), T.TTVector(xh)), EPS, host=True)
+            e2e_out[p] = z.cores
             return z
 
         e2e_out = {}

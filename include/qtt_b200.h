@@ -127,6 +127,15 @@ int qtt_scale(const qtt_layout* A, const double* a, double s, double* out,
  * qtt_layout_size(in) doubles (ranks never increase). */
 int qtt_round(const qtt_layout* in, const double* in_data, double eps,
               qtt_layout* out, double* out_data, void* stream);
+/* qtt_round that also streams the result to pinned host memory: every core is
+ * copied device -> host (at the same packed offsets as in out_data) on a
+ * second stream as soon as it is final, while the sweep continues, so the
+ * read-back overlaps the computation (the reference's tt_round returns host
+ * arrays; this is the drop-in's way of doing the same without a serial
+ * D2H pass).  host_data: page-locked, at least as large as out_data. */
+int qtt_round_to_host(const qtt_layout* in, const double* in_data, double eps,
+                      qtt_layout* out, double* out_data, double* host_data,
+                      void* stream);
 
 /* ------------------------------------------------------------------- (a6)
  * TT-SVD of a dense vector, replaces ttcore.tt_decompose for 1-D input

@@ -38,6 +38,7 @@ EXPORTS = (
     "qtt_transpose",
     "qtt_scale",
     "qtt_round",
+    "qtt_round_to_host",
     "qtt_decompose",
     "qtt_norm",
     "qtt_dot",

@@ -39,7 +39,7 @@ int transpose_tt(const qtt_layout*, const double*, const qtt_layout*, double*, c
 int scale_copy(const qtt_layout*, const double*, double, double*, cudaStream_t);
 int dot(const qtt_layout*, const double*, const qtt_layout*, const double*, double*, cudaStream_t);
 // round.cu
-int round_tt(const qtt_layout*, const double*, double, qtt_layout*, double*, cudaStream_t);
+int round_tt(const qtt_layout*, const double*, double, qtt_layout*, double*, cudaStream_t, double*);
 int norm_orth(const qtt_layout*, const double*, double*, cudaStream_t);
 int decompose(const double*, int, const int64_t*, double, qtt_layout*, double*, int64_t,
               cudaStream_t);
@@ -196,7 +196,14 @@ int qtt_round(const qtt_layout* in, const double* in_data, double eps, qtt_layou
               double* out_data, void* stream) {
   pool_init();
   if (!valid(in) || !out || eps < 0) return QTT_EINVAL;
-  return round_tt(in, in_data, eps, out, out_data, S(stream));
+  return round_tt(in, in_data, eps, out, out_data, S(stream), nullptr);
+}
+
+int qtt_round_to_host(const qtt_layout* in, const double* in_data, double eps, qtt_layout* out,
+                      double* out_data, double* host_data, void* stream) {
+  pool_init();
+  if (!valid(in) || !out || !host_data || eps < 0) return QTT_EINVAL;
+  return round_tt(in, in_data, eps, out, out_data, S(stream), host_data);
 }
 
 int qtt_decompose(const double* dense, int32_t d, const int64_t* sizes, double eps,

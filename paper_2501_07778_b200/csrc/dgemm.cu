@@ -334,6 +334,22 @@ void pool_init() {
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t thr = ~0ULL;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    // Cross-stream reuse policy.  Opportunistic reuse (the default) makes every
+    // allocation poll the completion of frees made on OTHER streams once several
+    // streams share the pool: after one concurrent step the ~15 workspace
+    // allocations of each CholeskyQR2 cost ~0.25 ms more (serial config-2 step
+    // 89 -> 115 ms, tools/scratch/serial_state_probe.py).  Internal
+    // dependencies would serialise the concurrent chains.  With 180 GB of HBM
+    // the pool simply grows instead: only stream-ordered / event-ordered reuse.
+    // QTT_POOL_REUSE overrides (bit 0: event deps, 1: opportunistic, 2: internal deps).
+    const char* e = getenv("QTT_POOL_REUSE");
+    const int bits = e ? atoi(e) : 1;
+    int v = bits & 1;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseFollowEventDependencies, &v);
+    v = (bits >> 1) & 1;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &v);
+    v = (bits >> 2) & 1;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &v);
   }
   done[dev] = true;
 }

@@ -40,6 +40,38 @@ struct DevBuf {
   }
 };
 
+}  // namespace
+
+// Progressive output of a rounding: every core is packed into out_data (at the
+// offsets qtt_layout uses: sizes rounded up to 32 doubles) as soon as it is
+// final and, when `host` is set, copied to pinned host memory on a second
+// stream while the sweep continues (qtt_round_to_host).
+struct CoreSink {
+  double* out_data = nullptr;
+  double* host = nullptr;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev = nullptr;
+  int64_t off = 0;
+  std::vector<int64_t> offs;
+  void reset(int d) {
+    off = 0;
+    offs.assign(d, 0);
+  }
+  int emit(cudaStream_t s, int k, int64_t size, const double* src) {
+    offs[k] = off;
+    QTT_CUDA(cudaMemcpyAsync(out_data + off, src, sizeof(double) * size, cudaMemcpyDeviceToDevice, s));
+    if (host) {
+      QTT_CUDA(cudaEventRecord(ev, s));
+      QTT_CUDA(cudaStreamWaitEvent(copy, ev, 0));
+      QTT_CUDA(cudaMemcpyAsync(host + off, out_data + off, sizeof(double) * size, cudaMemcpyDeviceToHost, copy));
+    }
+    off += (size + 31) / 32 * 32;
+    return kOk;
+  }
+};
+
+namespace {
+
 template <typename T>
 int fetch(cudaStream_t s, const T* dev, T* host) {
   QTT_CUDA(cudaMemcpyAsync(host, dev, sizeof(T), cudaMemcpyDeviceToHost, s));
@@ -187,7 +219,7 @@ int qr_cert_spec(cudaStream_t s, int m, int n, const double* A, int64_t lda, dou
 // rounding from its input with spec_failed == nullptr.
 int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vector<int64_t>& n,
                 const std::vector<int64_t>& off, double* work, double eps, int* spec_failed,
-                bool careful) {
+                bool careful, CoreSink* sink) {
   // careful: skip the CholeskyQR2 attempt for small factors (a thread whose
   // recent roundings met rank-deficient cores goes straight to Householder)
   if (spec_failed) *spec_failed = 0;
@@ -288,6 +320,8 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
   }
 
   const int first_bond = centre;
+  if (sink)  // the identity cores left of the centre are final
+    for (int j = 0; j < centre; ++j) QTT_TRY(sink->emit(s, j, r[j] * n[j] * r[j + 1], work + off[j]));
   for (int k = centre; k < d - 1; ++k) {
     const bool spec_k = spec_lr && k > first_bond;  // the first bond is examined
     const int m = (int)(r[k] * n[k]);
@@ -382,14 +416,16 @@ int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vecto
                              cudaMemcpyDeviceToDevice, s));
     pt.lap("lr-rest", k, m, N, newk);
     r[k + 1] = newk;
+    if (sink) QTT_TRY(sink->emit(s, k, r[k] * n[k] * newk, core));
   }
+  if (sink) QTT_TRY(sink->emit(s, d - 1, r[d - 1] * n[d - 1] * r[d], work + off[d - 1]));
   int bad = 0;
   QTT_TRY(spec_bad(&bad));
   return kOk;
 }
 
 int round_tt(const qtt_layout* in, const double* in_data, double eps, qtt_layout* out,
-             double* out_data, cudaStream_t s) {
+             double* out_data, cudaStream_t s, double* host_data) {
   const int d = in->d;
   if (d < 1 || d > QTT_MAX_CORES || eps < 0) return kInvalid;
   std::vector<int64_t> r(d + 1), n(d), off(d);
@@ -402,14 +438,32 @@ int round_tt(const qtt_layout* in, const double* in_data, double eps, qtt_layout
   DevBuf work;
   QTT_TRY(work.alloc(s, total));
   QTT_CUDA(cudaMemcpyAsync(work.p, in_data, sizeof(double) * total, cudaMemcpyDeviceToDevice, s));
+  // cores are packed into out_data (and streamed to the host) as they become final
+  thread_local cudaStream_t copy_stream = nullptr;
+  thread_local cudaEvent_t copy_ev = nullptr;
+  CoreSink sink;
+  sink.out_data = out_data;
+  if (host_data) {
+    if (!copy_stream) {
+      QTT_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+      QTT_CUDA(cudaEventCreateWithFlags(&copy_ev, cudaEventDisableTiming));
+    }
+    sink.host = host_data;
+    sink.copy = copy_stream;
+    sink.ev = copy_ev;
+  }
+  sink.reset(d);
   // Speculate "every small factor is well conditioned" (true for products of
   // random / full-rank TTs such as BASELINE configs 2 and 3).
   static const bool spec_on = getenv("QTT_ROUND_NO_SPEC") == nullptr;
   thread_local int cooldown = 0;
   bool done = false, careful = false;
-  if (spec_on && cooldown == 0) {
+  if (d == 1) {
+    QTT_TRY(sink.emit(s, 0, r[0] * n[0] * r[1], work.p + off[0]));
+    done = true;
+  } else if (spec_on && cooldown == 0) {
     int failed = 0;
-    QTT_TRY(round_slots(s, d, r, n, off, work.p, eps, &failed, false));
+    QTT_TRY(round_slots(s, d, r, n, off, work.p, eps, &failed, false, &sink));
     if (!failed) {
       done = true;
     } else {
@@ -420,20 +474,20 @@ int round_tt(const qtt_layout* in, const double* in_data, double eps, qtt_layout
       careful = true;
       for (int k = 0; k <= d; ++k) r[k] = in->ranks[k];
       QTT_CUDA(cudaMemcpyAsync(work.p, in_data, sizeof(double) * total, cudaMemcpyDeviceToDevice, s));
+      sink.reset(d);
     }
   } else if (cooldown > 0) {
     --cooldown;
     careful = true;
   }
-  if (!done) QTT_TRY(round_slots(s, d, r, n, off, work.p, eps, nullptr, careful));
+  if (!done) QTT_TRY(round_slots(s, d, r, n, off, work.p, eps, nullptr, careful, &sink));
   *out = *in;
   for (int k = 0; k <= d; ++k) out->ranks[k] = r[k];
   pack_offsets(out);
   for (int k = 0; k < d; ++k)
-    QTT_CUDA(cudaMemcpyAsync(out_data + out->offsets[k], work.p + off[k],
-                             sizeof(double) * r[k] * n[k] * r[k + 1], cudaMemcpyDeviceToDevice,
-                             s));
+    if (out->offsets[k] != sink.offs[k]) return kInvalid;  // the sink packs exactly as qtt_layout does
   QTT_CUDA(cudaStreamSynchronize(s));
+  if (host_data) QTT_CUDA(cudaStreamSynchronize(copy_stream));
   return kOk;
 }
 

@@ -367,9 +367,14 @@ def tt_contract(t) -> np.ndarray:
 # ------------------------------------------------------------- rounding
 
 
-def tt_round(t, epsilon: float):
+def tt_round(t, epsilon: float, host: bool = False):
     """Compress at relative tolerance epsilon; ranks never increase
-    (ttcore.py:322-338)."""
+    (ttcore.py:322-338).
+
+    ``host=True`` (extension): the cores are also streamed to pinned host
+    memory while the sweep runs (``qtt_round_to_host``), so ``.cores`` of the
+    result -- host arrays, as the reference returns them -- costs no separate
+    device-to-host pass."""
     if epsilon < 0:
         raise ValueError("epsilon must be >= 0")
     if not _is_tt(t):
@@ -377,9 +382,31 @@ def tt_round(t, epsilon: float):
     lay = t._layout()
     out_lay = _lib.Layout()
     out = torch.empty_like(t.data)
-    _lib.call("qtt_round", ctypes.byref(lay), _lib.ptr(t.data), ctypes.c_double(epsilon),
-              ctypes.byref(out_lay), _lib.ptr(out), _S())
-    return _from_layout(type(t), out_lay, out)
+    if not host:
+        _lib.call("qtt_round", ctypes.byref(lay), _lib.ptr(t.data), ctypes.c_double(epsilon),
+                  ctypes.byref(out_lay), _lib.ptr(out), _S())
+        return _from_layout(type(t), out_lay, out)
+    # ranks never exceed the structural bounds: a tight capacity for the pinned buffer
+    ranks = list(t.ranks)
+    sizes = [int(np.prod(s[1:-1])) for s in t._shapes]
+    left = right = 1
+    for k in range(1, len(ranks) - 1):
+        left *= sizes[k - 1]
+        ranks[k] = min(ranks[k], left)
+    for k in range(len(ranks) - 2, 0, -1):
+        right *= sizes[k]
+        ranks[k] = min(ranks[k], right)
+    cap = sum(_lib.align(ranks[k] * sizes[k] * ranks[k + 1]) for k in range(len(sizes)))
+    hbuf = torch.empty(max(cap, 1), dtype=torch.float64, pin_memory=True)
+    _lib.call("qtt_round_to_host", ctypes.byref(lay), _lib.ptr(t.data), ctypes.c_double(epsilon),
+              ctypes.byref(out_lay), _lib.ptr(out), ctypes.c_void_p(hbuf.data_ptr()), _S())
+    res = _from_layout(type(t), out_lay, out)
+    hv = hbuf.numpy()
+    cores = tuple(hv[o : o + int(np.prod(s))].reshape(s) for o, s in zip(res._offs, res._shapes))
+    for a in cores:
+        a.flags.writeable = False
+    res._host = cores
+    return res
 
 
 def tt_norm(t) -> float:

@@ -275,6 +275,44 @@ def test_round_speculation_recovers(where):
         assert err <= 1e-10 * (1 + 1e-8) + 1e-13
 
 
+@pytest.mark.parametrize("case", ["full", "truncating", "deficient"])
+def test_round_streams_cores_to_host(case):
+    """tt_round(host=True) (qtt_round_to_host): the cores streamed to pinned
+    host memory during the sweep equal the device result bit for bit, for a
+    full-rank product, a truncating sum and a rank-deficient input that sends
+    the speculative sweep back to the examined path."""
+    T = _T()
+    rng = np.random.default_rng({"full": 21, "truncating": 22, "deficient": 23}[case])
+    if case == "full":
+        d, r = 12, 48
+        rk = [1] + [min(r, 2**k, 2 ** (d - k)) for k in range(1, d)] + [1]
+        cores = [rng.standard_normal((rk[k], 2, rk[k + 1])) for k in range(d)]
+    elif case == "truncating":
+        x = rand_vec(rng, 9, 5)
+        cores = O.add(O.add(x, O.scale(x, 0.25)), rand_vec(rng, 9, 3))
+    else:
+        d, r = 13, 64
+        rk = [1] + [min(r, 2**k, 2 ** (d - k)) for k in range(1, d)] + [1]
+        cores = [rng.standard_normal((rk[k], 2, rk[k + 1])) / 8 for k in range(d)]
+        a, n, b = cores[6].shape
+        cores[6] = (rng.standard_normal((a * n, 9)) @ rng.standard_normal((9, b))).reshape(a, n, b)
+    t = T.TTVector(cores)
+    full = O.full(cores)
+    for rep in range(2):
+        dev = T.tt_round(t, 1e-9)
+        hst = T.tt_round(t, 1e-9, host=True)
+        assert hst.ranks == dev.ranks
+        # the streamed host cores are the device cores, bit for bit
+        for a, c in zip(hst.cores, hst.numpy_cores()):
+            assert isinstance(a, np.ndarray) and not a.flags.writeable
+            assert np.array_equal(a, c)
+        # (two separate roundings may differ in gauge: the calling thread's
+        # speculation cool-down picks CholeskyQR2 or Householder factors)
+        got = O.full([np.array(a) for a in hst.cores])
+        assert np.linalg.norm(got - full) <= 1e-9 * (1 + 1e-6) * np.linalg.norm(full)
+        assert np.linalg.norm(got - dense_of(dev)) <= 1e-12 * np.linalg.norm(full)
+
+
 def test_round_matrix():
     T = _T()
     rng = np.random.default_rng(5)
