@@ -75,6 +75,11 @@ int64_t qtt_layout_size(const qtt_layout* lay);
  * stream-ordered pool to the driver (no reference counterpart: host-side
  * memory management for growing AMEn local systems, solver.py:148-171). */
 int qtt_release_cached(void* stream);
+/* Memory-pool policy of the CALLING host thread for the library's
+ * stream-ordered temporaries: 1 = the device's shared default pool (what the
+ * concurrent chain workers of the Python mirror use), 0 = a pool private to
+ * the thread (the default; see csrc/common.cuh for the measurements). */
+int qtt_thread_shared_pool(int32_t shared);
 
 /* ---------------------------------------------------------------- (a2,a3)
  * Exact core-wise products, all cores in ONE launch.

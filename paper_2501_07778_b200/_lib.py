@@ -29,6 +29,7 @@ EXPORTS = (
     "qtt_profile_gemm_shape",
     "qtt_layout_size",
     "qtt_release_cached",
+    "qtt_thread_shared_pool",
     "qtt_matvec",
     "qtt_matmat",
     "qtt_hadamard",
@@ -178,8 +179,40 @@ def gemm_profile_shapes(count: int) -> list:
     return out
 
 
-_POOL = None
+_WORKERS: list = []
 _STREAMS: list = []
+
+
+class _Worker:
+    """One host thread bound to one chain slot: slot i always runs on thread i
+    with stream i, so the library's per-thread state (private memory pool,
+    look-ahead side stream, speculation cool-down) stays with the chain."""
+
+    def __init__(self, idx: int):
+        import queue
+        import threading
+
+        self.q = queue.SimpleQueue()
+        self.t = threading.Thread(target=self._loop, name=f"qtt-chain-{idx}", daemon=True)
+        self.t.start()
+
+    def _loop(self):
+        # concurrent chains share the device's default pool (fastest while they
+        # all run); the caller's thread keeps its private pool (csrc/common.cuh)
+        load().qtt_thread_shared_pool(ctypes.c_int32(1))
+        while True:
+            fut, fn, args = self.q.get()
+            if not fut.set_running_or_notify_cancel():
+                continue
+            try:
+                fut.set_result(fn(*args))
+            except BaseException as exc:  # delivered to the submitting thread
+                fut.set_exception(exc)
+
+    def submit(self, fn, *args):
+        fut = concurrent.futures.Future()
+        self.q.put((fut, fn, args))
+        return fut
 
 
 def run_concurrent(jobs):
@@ -188,10 +221,15 @@ def run_concurrent(jobs):
     host synchronisations then overlap the others' kernels).  Inputs were
     produced on the caller's stream, which every chain stream waits for; the
     caller's stream waits for all chains before the results are used."""
-    global _POOL, _STREAMS
+    global _WORKERS, _STREAMS
+    import threading
+
+    if threading.current_thread().name.startswith("qtt-chain-"):
+        # nested use from inside a chain: its own slot would wait on itself
+        return [fn(arg) for fn, arg in jobs]
     dev = torch.cuda.current_device()
-    if _POOL is None:
-        _POOL = concurrent.futures.ThreadPoolExecutor(max_workers=12, thread_name_prefix="qtt-chain")
+    while len(_WORKERS) < len(jobs):
+        _WORKERS.append(_Worker(len(_WORKERS)))
     if len(_STREAMS) < len(jobs) or _STREAMS[0].device.index != dev:
         # callers order their jobs longest first: the earlier a chain, the
         # higher its stream priority, so the critical (longest) chain is not
@@ -218,7 +256,7 @@ def run_concurrent(jobs):
                 t.record_stream(main)
         return out
 
-    futs = [_POOL.submit(run, fn, arg, _STREAMS[i]) for i, (fn, arg) in enumerate(jobs)]
+    futs = [_WORKERS[i].submit(run, fn, arg, _STREAMS[i]) for i, (fn, arg) in enumerate(jobs)]
     # wait for EVERY chain before joining the streams: if one job raises, the
     # others must not keep reading or writing memory the caller may free
     concurrent.futures.wait(futs)

@@ -133,6 +133,13 @@ int qtt_release_cached(void* stream) {
   cudaMemPool_t pool;
   QTT_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
   QTT_CUDA(cudaMemPoolTrimTo(pool, 0));
+  trim_thread_pools();
+  return QTT_OK;
+}
+
+int qtt_thread_shared_pool(int32_t shared) {
+  pool_init();
+  set_thread_shared_pool(shared != 0);
   return QTT_OK;
 }
 
@@ -296,14 +303,14 @@ int qtt_svd(int64_t m, int64_t n, const double* a, int64_t lda, double* s, doubl
   double *Q = nullptr, *R = nullptr, *X = nullptr, *W = nullptr, *tmp = nullptr;
   int* perm = nullptr;
   int* rank = nullptr;
-  QTT_CUDA(cudaMallocAsync(&R, sizeof(double) * (int64_t)k * std::max(M, N), st));
-  QTT_CUDA(cudaMallocAsync(&X, sizeof(double) * (int64_t)k * k, st));
-  QTT_CUDA(cudaMallocAsync(&W, sizeof(double) * (int64_t)k * k, st));
-  QTT_CUDA(cudaMallocAsync(&perm, sizeof(int) * (k + 2), st));
+  QTT_CUDA(malloc_async(&R, sizeof(double) * (int64_t)k * std::max(M, N), st));
+  QTT_CUDA(malloc_async(&X, sizeof(double) * (int64_t)k * k, st));
+  QTT_CUDA(malloc_async(&W, sizeof(double) * (int64_t)k * k, st));
+  QTT_CUDA(malloc_async(&perm, sizeof(int) * (k + 2), st));
   rank = perm + k;
   if (M >= N) {
-    QTT_CUDA(cudaMallocAsync(&Q, sizeof(double) * (int64_t)M * k, st));
-    QTT_CUDA(cudaMallocAsync(&tmp, sizeof(double) * (int64_t)M * k, st));
+    QTT_CUDA(malloc_async(&Q, sizeof(double) * (int64_t)M * k, st));
+    QTT_CUDA(malloc_async(&tmp, sizeof(double) * (int64_t)M * k, st));
     QTT_TRY(qr(st, M, N, a, lda, Q, M, R, k, nullptr, true));  // SVD inputs are ill-conditioned by design
     QTT_TRY(transpose(st, k, k, R, k, X, k));
     QTT_TRY(jacobi(st, k, k, X, k, W, k));
@@ -313,7 +320,7 @@ int qtt_svd(int64_t m, int64_t n, const double* a, int64_t lda, double* s, doubl
     QTT_CUDA(cudaFreeAsync(Q, st));
     QTT_CUDA(cudaFreeAsync(tmp, st));
   } else {
-    QTT_CUDA(cudaMallocAsync(&tmp, sizeof(double) * (int64_t)M * N, st));
+    QTT_CUDA(malloc_async(&tmp, sizeof(double) * (int64_t)M * N, st));
     QTT_TRY(transpose(st, M, N, a, lda, tmp, N));
     QTT_TRY(qr(st, N, M, tmp, N, nullptr, 1, R, k, nullptr, true));
     QTT_TRY(copy_matrix(st, k, k, R, k, X, k));

@@ -897,11 +897,11 @@ int gram_certificate(cudaStream_t s, int p, int r, const double* X, int64_t ldx,
   const int64_t nn = r;
   double *G, *Ri, *rblk, *sc;
   int* bad;
-  QTT_CUDA(cudaMallocAsync(&G, sizeof(double) * nn * nn, s));
-  QTT_CUDA(cudaMallocAsync(&Ri, sizeof(double) * nn * nn, s));
-  QTT_CUDA(cudaMallocAsync(&rblk, sizeof(double) * CB * CB * ceil_div(nn, CB), s));
-  QTT_CUDA(cudaMallocAsync(&sc, sizeof(double) * 4, s));
-  QTT_CUDA(cudaMallocAsync(&bad, sizeof(int), s));
+  QTT_CUDA(malloc_async(&G, sizeof(double) * nn * nn, s));
+  QTT_CUDA(malloc_async(&Ri, sizeof(double) * nn * nn, s));
+  QTT_CUDA(malloc_async(&rblk, sizeof(double) * CB * CB * ceil_div(nn, CB), s));
+  QTT_CUDA(malloc_async(&sc, sizeof(double) * 4, s));
+  QTT_CUDA(malloc_async(&bad, sizeof(int), s));
   QTT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
   int status = kOk;
   do {
@@ -933,8 +933,8 @@ int cholqr2_small(cudaStream_t s, int m, int n, const double* A, int64_t lda, do
   if (m < n || n <= 0 || n > 2 * kBlk) return kInvalid;
   const int64_t nn = n;
   double *buf, *Q1;
-  QTT_CUDA(cudaMallocAsync(&buf, sizeof(double) * (4 * nn * nn + 8), s));
-  QTT_CUDA(cudaMallocAsync(&Q1, sizeof(double) * (int64_t)m * nn, s));
+  QTT_CUDA(malloc_async(&buf, sizeof(double) * (4 * nn * nn + 8), s));
+  QTT_CUDA(malloc_async(&Q1, sizeof(double) * (int64_t)m * nn, s));
   double *G = buf, *R1 = buf + nn * nn, *Ri = buf + 2 * nn * nn, *R2 = buf + 3 * nn * nn,
          *sc = scalars ? scalars : buf + 4 * nn * nn;
   int status_code = kOk;
@@ -971,14 +971,14 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
   const int64_t nn = n;
   double *G, *R1, *Ri, *Q1, *rblk, *scal, *parts;
   int* bad;
-  QTT_CUDA(cudaMallocAsync(&G, sizeof(double) * nn * nn, s));
-  QTT_CUDA(cudaMallocAsync(&R1, sizeof(double) * nn * nn, s));
-  QTT_CUDA(cudaMallocAsync(&Ri, sizeof(double) * nn * nn, s));
-  QTT_CUDA(cudaMallocAsync(&Q1, sizeof(double) * (int64_t)m * nn, s));
-  QTT_CUDA(cudaMallocAsync(&rblk, sizeof(double) * CB * CB * ceil_div(nn, CB), s));
-  QTT_CUDA(cudaMallocAsync(&scal, sizeof(double) * 4, s));
-  QTT_CUDA(cudaMallocAsync(&parts, sizeof(double) * kDefectParts, s));
-  QTT_CUDA(cudaMallocAsync(&bad, sizeof(int), s));
+  QTT_CUDA(malloc_async(&G, sizeof(double) * nn * nn, s));
+  QTT_CUDA(malloc_async(&R1, sizeof(double) * nn * nn, s));
+  QTT_CUDA(malloc_async(&Ri, sizeof(double) * nn * nn, s));
+  QTT_CUDA(malloc_async(&Q1, sizeof(double) * (int64_t)m * nn, s));
+  QTT_CUDA(malloc_async(&rblk, sizeof(double) * CB * CB * ceil_div(nn, CB), s));
+  QTT_CUDA(malloc_async(&scal, sizeof(double) * 4, s));
+  QTT_CUDA(malloc_async(&parts, sizeof(double) * kDefectParts, s));
+  QTT_CUDA(malloc_async(&bad, sizeof(int), s));
   QTT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
   int status = kOk;
   PhaseTimer pt(s);
@@ -1019,8 +1019,8 @@ int cholqr2(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* 
       int iters = 0;
       while (iters < 8 && std::pow(std::max(delta, 1e-300), iters + 2) > 1e-17) ++iters;
       double *U, *W;
-      QTT_CUDA(cudaMallocAsync(&U, sizeof(double) * nn * nn, s));
-      QTT_CUDA(cudaMallocAsync(&W, sizeof(double) * nn * nn, s));
+      QTT_CUDA(malloc_async(&U, sizeof(double) * nn * nn, s));
+      QTT_CUDA(malloc_async(&W, sizeof(double) * nn * nn, s));
       status = chol_near_identity(s, n, G, nn, U, W, iters);
       QTT_CUDA(cudaFreeAsync(U, s));
       QTT_CUDA(cudaFreeAsync(W, s));

@@ -269,6 +269,33 @@ constexpr int kGemmUpperC = 1, kGemmTriA = 2, kGemmTriB = 4, kGemmLowA = 8, kGem
 
 int gemm(const GemmArgs& g, cudaStream_t stream);
 
+// Stream-ordered allocation of library temporaries.  Two kinds of host
+// thread use the library: the chain workers of run_concurrent (one thread +
+// stream per independent TT problem, all alive at once) and everything else
+// (the caller's thread: serial roundings, the AMEn sweep).  Measured on the
+// config-2 step (tools/scratch/serial_state_probe.py, QTT_SHARED_POOL A/B):
+// * the chain workers are fastest on the device's SHARED default pool with
+//   its opportunistic cross-stream reuse (44.7 ms per concurrent step; 46-47
+//   ms on private pools or without opportunistic reuse: blocks just freed by
+//   a neighbour chain are still in L2);
+// * but once those chains have populated the shared pool, every allocation
+//   made on another thread polls the completion of their frees: the ~15
+//   workspace allocations of each CholeskyQR2 cost ~0.25 ms more (serial
+//   step 89 -> 115 ms, constant-E solve 2.9 -> 3.3 s).
+// So worker threads opt in to the shared pool (qtt_thread_shared_pool) and
+// every other thread allocates from a pool PRIVATE to it (one per device,
+// created on first use, release threshold = max).  cudaFreeAsync returns a
+// block to the pool it came from, whichever thread frees it.
+cudaError_t malloc_async(void** p, size_t bytes, cudaStream_t s);
+template <typename T>
+inline cudaError_t malloc_async(T** p, size_t bytes, cudaStream_t s) {
+  return malloc_async(reinterpret_cast<void**>(p), bytes, s);
+}
+// Trim every pool created by malloc_async (qtt_release_cached).
+void trim_thread_pools();
+// The calling thread allocates from the device's shared default pool from now on.
+void set_thread_shared_pool(bool shared);
+
 // Keep freed stream-ordered allocations cached in the device's default pool
 // (release threshold = max): the TT sweeps allocate and free workspaces on
 // every step, and trimming the pool at each synchronisation would re-map

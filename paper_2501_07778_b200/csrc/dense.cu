@@ -78,8 +78,8 @@ int contract_merged(const qtt_layout* L, const double* a, double* out, cudaStrea
     maxbuf = std::max(maxbuf, total * L->ranks[l + 1]);
   }
   double *b0, *b1;
-  QTT_CUDA(cudaMallocAsync(&b0, sizeof(double) * maxbuf, s));
-  QTT_CUDA(cudaMallocAsync(&b1, sizeof(double) * maxbuf, s));
+  QTT_CUDA(malloc_async(&b0, sizeof(double) * maxbuf, s));
+  QTT_CUDA(malloc_async(&b1, sizeof(double) * maxbuf, s));
   QTT_TRY(fill(s, b0, 1, 1.0));
   double* cur = b0;
   double* nxt = b1;
@@ -114,7 +114,7 @@ int contract(const qtt_layout* L, const double* a, double* dense, cudaStream_t s
   if (bits > 26) return kUnsupported;
   if (!L->is_matrix) return contract_merged(L, a, dense, s);
   double* merged;
-  QTT_CUDA(cudaMallocAsync(&merged, sizeof(double) * rows * cols, s));
+  QTT_CUDA(malloc_async(&merged, sizeof(double) * rows * cols, s));
   QTT_TRY(contract_merged(L, a, merged, s));
   MatPerm mp;
   mp.d = d;
@@ -168,9 +168,9 @@ int dense_apply(const qtt_layout* LA, const double* a, const double* v, double* 
   for (int l = 0; l < d; ++l)
     maxcore = std::max(maxcore, LA->ranks[l] * LA->rows[l] * LA->cols[l] * LA->ranks[l + 1]);
   double *b0, *b1, *apk;
-  QTT_CUDA(cudaMallocAsync(&b0, sizeof(double) * maxbuf, s));
-  QTT_CUDA(cudaMallocAsync(&b1, sizeof(double) * maxbuf, s));
-  QTT_CUDA(cudaMallocAsync(&apk, sizeof(double) * maxcore, s));
+  QTT_CUDA(malloc_async(&b0, sizeof(double) * maxbuf, s));
+  QTT_CUDA(malloc_async(&b1, sizeof(double) * maxbuf, s));
+  QTT_CUDA(malloc_async(&apk, sizeof(double) * maxcore, s));
   QTT_CUDA(cudaMemcpyAsync(b0, v, sizeof(double) * cols, cudaMemcpyDeviceToDevice, s));
   double* cur = b0;
   double* nxt = b1;

@@ -334,24 +334,50 @@ void pool_init() {
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t thr = ~0ULL;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    // Cross-stream reuse policy.  Opportunistic reuse (the default) makes every
-    // allocation poll the completion of frees made on OTHER streams once several
-    // streams share the pool: after one concurrent step the ~15 workspace
-    // allocations of each CholeskyQR2 cost ~0.25 ms more (serial config-2 step
-    // 89 -> 115 ms, tools/scratch/serial_state_probe.py).  Internal
-    // dependencies would serialise the concurrent chains.  With 180 GB of HBM
-    // the pool simply grows instead: only stream-ordered / event-ordered reuse.
-    // QTT_POOL_REUSE overrides (bit 0: event deps, 1: opportunistic, 2: internal deps).
-    const char* e = getenv("QTT_POOL_REUSE");
-    const int bits = e ? atoi(e) : 1;
-    int v = bits & 1;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseFollowEventDependencies, &v);
-    v = (bits >> 1) & 1;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &v);
-    v = (bits >> 2) & 1;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &v);
   }
   done[dev] = true;
+}
+
+namespace {
+std::mutex g_pool_mu;
+std::vector<cudaMemPool_t> g_pools;
+}  // namespace
+
+namespace {
+thread_local bool t_shared_pool = false;
+}  // namespace
+
+void set_thread_shared_pool(bool shared) { t_shared_pool = shared; }
+
+cudaError_t malloc_async(void** p, size_t bytes, cudaStream_t s) {
+  // QTT_SHARED_POOL=1 / =0: every thread on the device's default pool / on a private one (A/B)
+  static const char* env = getenv("QTT_SHARED_POOL");
+  const bool shared = env ? env[0] != '0' : t_shared_pool;
+  if (shared) return cudaMallocAsync(p, bytes, s);
+  thread_local cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  dev &= 63;
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    e = cudaMemPoolCreate(&pools[dev], &props);
+    if (e != cudaSuccess) return e;
+    uint64_t thr = ~0ULL;
+    cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pools.push_back(pools[dev]);
+  }
+  return cudaMallocFromPoolAsync(p, bytes, pools[dev], s);
+}
+
+void trim_thread_pools() {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (cudaMemPool_t pool : g_pools) cudaMemPoolTrimTo(pool, 0);
 }
 
 GemmProfile& gemm_profile() {
@@ -407,7 +433,7 @@ int gemm(const GemmArgs& g, cudaStream_t stream) {
   if (splits > 1) splits = (int)ceil_div(g.k, kchunk);
   double* ws = nullptr;
   if (splits > 1)
-    QTT_CUDA(cudaMallocAsync(&ws, sizeof(double) * splits * g.batch * (int64_t)g.m * g.n, stream));
+    QTT_CUDA(malloc_async(&ws, sizeof(double) * splits * g.batch * (int64_t)g.m * g.n, stream));
   grid.z = splits;
   static DeviceFlag configured;
   if (!configured.test()) {

@@ -143,7 +143,7 @@ extern "C" int qtt_element_grids(int32_t d, int32_t zorder, int32_t ngauss, cons
   for (int r = 0; r < 3; ++r)
     for (int c = 0; c < 3; ++c) ec.C[r][c] = cmat[3 * r + c];
   int* flag;
-  QTT_CUDA(cudaMallocAsync(&flag, sizeof(int), s));
+  QTT_CUDA(malloc_async(&flag, sizeof(int), s));
   QTT_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
   const int64_t total = (1LL << (2 * d)) * 4;
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 16 * num_sms()));

@@ -223,7 +223,7 @@ struct DevMem {
   std::vector<std::pair<void*, cudaStream_t>> v;
   template <typename T>
   int get(cudaStream_t s, T** p, int64_t n) {
-    QTT_CUDA(cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * std::max<int64_t>(n, 1), s));
+    QTT_CUDA(malloc_async(reinterpret_cast<void**>(p), sizeof(T) * std::max<int64_t>(n, 1), s));
     v.emplace_back(*p, s);
     return kOk;
   }
@@ -385,8 +385,8 @@ extern "C" int qtt_local_gmres(int64_t rl, int64_t n, int64_t rr, int64_t ra, in
   if (dim > 0x7fffffff || work > ((int64_t)1 << 40)) return QTT_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   double *t1 = nullptr, *p1 = nullptr;
-  QTT_CUDA(cudaMallocAsync(&t1, sizeof(double) * work, s));
-  QTT_CUDA(cudaMallocAsync(&p1, sizeof(double) * work, s));
+  QTT_CUDA(qtt::malloc_async(&t1, sizeof(double) * work, s));
+  QTT_CUDA(qtt::malloc_async(&p1, sizeof(double) * work, s));
   qtt::LocalOp op{rl, n, rr, ra, rb, phi_l, a_jib, phi_r, t1, p1};
   int it = 0, conv = 0;
   const int st = qtt::local_gmres(s, op, rhs, x0, x, rtol, restart, maxit, abort_early, &it, &conv);
@@ -405,8 +405,8 @@ extern "C" int qtt_local_apply(int64_t rl, int64_t n, int64_t rr, int64_t ra, in
   const int64_t work = std::max(rl * ra * n * rr, rl * rr * n * rb);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   double *t1 = nullptr, *p1 = nullptr;
-  QTT_CUDA(cudaMallocAsync(&t1, sizeof(double) * work, s));
-  QTT_CUDA(cudaMallocAsync(&p1, sizeof(double) * work, s));
+  QTT_CUDA(qtt::malloc_async(&t1, sizeof(double) * work, s));
+  QTT_CUDA(qtt::malloc_async(&p1, sizeof(double) * work, s));
   qtt::LocalOp op{rl, n, rr, ra, rb, phi_l, a_jib, phi_r, t1, p1};
   const int st = qtt::local_apply(s, op, x, y);
   cudaFreeAsync(t1, s);

@@ -1127,7 +1127,7 @@ int jacobi_gring(cudaStream_t s, int p, int k, double* X, int64_t ldx, double* W
     configured.set();
   }
   double* slots;
-  QTT_CUDA(cudaMallocAsync(&slots, sizeof(double) * 4 * (size_t)np * ((size_t)p + k), s));
+  QTT_CUDA(malloc_async(&slots, sizeof(double) * 4 * (size_t)np * ((size_t)p + k), s));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs, 1, 1);
   cfg.blockDim = dim3(ppc * 32, 1, 1);
@@ -1517,7 +1517,7 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
   if (use_cq_small && !careful && m >= n && n >= kCholQrSmallMin && n <= kCholQrSmallMax) {
     if (spec_dev) return cholqr2_small(s, m, n, A, lda, Q, ldq, R, ldr, spec_dev);
     int* st;
-    QTT_CUDA(cudaMallocAsync(&st, sizeof(int), s));
+    QTT_CUDA(malloc_async(&st, sizeof(int), s));
     QTT_CUDA(cudaMemsetAsync(st, 0, sizeof(int), s));
     QTT_TRY(cholqr2_small(s, m, n, A, lda, Q, ldq, R, ldr, st));
     int hst = 0;
@@ -1532,7 +1532,7 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
   static const bool use_chol = getenv("QTT_NO_CHOLQR") == nullptr;
   if (use_chol && m >= n && n >= 128) {
     double* Rt = R;
-    if (!R) QTT_CUDA(cudaMallocAsync(&Rt, sizeof(double) * (int64_t)n * n, s));
+    if (!R) QTT_CUDA(malloc_async(&Rt, sizeof(double) * (int64_t)n * n, s));
     int ok = 0;
     QTT_TRY(cholqr2(s, m, n, A, lda, Q, Q ? ldq : m, Rt, R ? ldr : n, &ok, info));  // Q may be null (R only)
     if (!R) QTT_CUDA(cudaFreeAsync(Rt, s));
@@ -1544,13 +1544,13 @@ int qr(cudaStream_t s, int m, int n, const double* A, int64_t lda, double* Q, in
   const int PW = panel_width(m);
   double *Ac, *V, *Y, *Y2, *tau, *W, *W1;
   const int64_t mm = m;
-  QTT_CUDA(cudaMallocAsync(&Ac, sizeof(double) * mm * n, s));
-  QTT_CUDA(cudaMallocAsync(&V, sizeof(double) * mm * k, s));
-  QTT_CUDA(cudaMallocAsync(&Y, sizeof(double) * mm * k, s));
-  QTT_CUDA(cudaMallocAsync(&Y2, sizeof(double) * mm * k, s));
-  QTT_CUDA(cudaMallocAsync(&tau, sizeof(double) * (k + 1), s));
-  QTT_CUDA(cudaMallocAsync(&W, sizeof(double) * PW * (int64_t)std::max(n, k), s));
-  QTT_CUDA(cudaMallocAsync(&W1, sizeof(double) * PW * PW, s));
+  QTT_CUDA(malloc_async(&Ac, sizeof(double) * mm * n, s));
+  QTT_CUDA(malloc_async(&V, sizeof(double) * mm * k, s));
+  QTT_CUDA(malloc_async(&Y, sizeof(double) * mm * k, s));
+  QTT_CUDA(malloc_async(&Y2, sizeof(double) * mm * k, s));
+  QTT_CUDA(malloc_async(&tau, sizeof(double) * (k + 1), s));
+  QTT_CUDA(malloc_async(&W, sizeof(double) * PW * (int64_t)std::max(n, k), s));
+  QTT_CUDA(malloc_async(&W1, sizeof(double) * PW * PW, s));
   QTT_TRY(copy_matrix(s, m, n, A, lda, Ac, m));
   // Look-ahead: after panel p, update only panel p+1's columns, factor panel
   // p+1 on a side stream while the rest of the trailing matrix is updated,
@@ -1718,7 +1718,7 @@ static int jacobi_impl(cudaStream_t s, int p, int k, double* X, int64_t ldx, dou
   }
   QTT_TRY(set_identity(s, k, k, W, ldw));
   int* flags;
-  QTT_CUDA(cudaMallocAsync(&flags, sizeof(int) * JMAXSWEEPS, s));
+  QTT_CUDA(malloc_async(&flags, sizeof(int) * JMAXSWEEPS, s));
   QTT_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * JMAXSWEEPS, s));
   int dev = 0, per_sm = 0;
   QTT_CUDA(cudaGetDevice(&dev));
@@ -1753,7 +1753,7 @@ int sort_chop(cudaStream_t s, int p, int k, const double* X, int64_t ldx, double
 int frob_norm(cudaStream_t s, int64_t n, const double* x, double* out_dev) {
   const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 1024), 1024));
   double* part;
-  QTT_CUDA(cudaMallocAsync(&part, sizeof(double) * parts, s));
+  QTT_CUDA(malloc_async(&part, sizeof(double) * parts, s));
   sumsq_partial_kernel<<<parts, 256, 0, s>>>(n, x, part);
   QTT_CHECK_LAUNCH();
   sum_final_kernel<<<1, 1024, 0, s>>>(parts, part, out_dev, 1);
@@ -1765,7 +1765,7 @@ int frob_norm(cudaStream_t s, int64_t n, const double* x, double* out_dev) {
 int tri_inverse(cudaStream_t s, int k, const double* R, int64_t ldr, double* X) {
   double* T;
   const int64_t kk = k;
-  QTT_CUDA(cudaMallocAsync(&T, sizeof(double) * kk * kk, s));
+  QTT_CUDA(malloc_async(&T, sizeof(double) * kk * kk, s));
   QTT_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * kk * kk, s));
   static DeviceFlag configured;
   const int tri_smem = (int)((kBlk * (kBlk + 1) + 256 + kBlk) * sizeof(double));
@@ -1817,12 +1817,12 @@ int no_truncation_certificate(cudaStream_t s, int k, const double* R, int64_t ld
   if (use_small && k <= 2 * kBlk) return cert_small(s, k, R, ldr, delta_dev, delta_scale, ok_dev, nullptr);
   double *X, *norms;
   const int64_t kk = k;
-  QTT_CUDA(cudaMallocAsync(&X, sizeof(double) * kk * kk, s));
-  QTT_CUDA(cudaMallocAsync(&norms, sizeof(double) * 2, s));
+  QTT_CUDA(malloc_async(&X, sizeof(double) * kk * kk, s));
+  QTT_CUDA(malloc_async(&norms, sizeof(double) * 2, s));
   QTT_TRY(tri_inverse(s, k, R, ldr, X));
   // ||R||_F (upper triangle of R as stored: caller guarantees zeros below)
   double* Rc;
-  QTT_CUDA(cudaMallocAsync(&Rc, sizeof(double) * kk * kk, s));
+  QTT_CUDA(malloc_async(&Rc, sizeof(double) * kk * kk, s));
   QTT_TRY(copy_matrix(s, k, k, R, ldr, Rc, kk));
   QTT_TRY(frob_norm(s, kk * kk, Rc, norms));
   QTT_TRY(frob_norm(s, kk * kk, X, norms + 1));

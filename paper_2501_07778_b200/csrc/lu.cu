@@ -291,13 +291,13 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
   const int nblk = (int)ceil_div(N, LB);
   double *A, *linv, *uinv, *tmp, *r, *nrm;
   int* bad;
-  QTT_CUDA(cudaMallocAsync(&A, sizeof(double) * ld * (N + 1), s));
-  QTT_CUDA(cudaMallocAsync(&linv, sizeof(double) * LB * LB * nblk, s));
-  QTT_CUDA(cudaMallocAsync(&uinv, sizeof(double) * LB * LB * nblk, s));
+  QTT_CUDA(malloc_async(&A, sizeof(double) * ld * (N + 1), s));
+  QTT_CUDA(malloc_async(&linv, sizeof(double) * LB * LB * nblk, s));
+  QTT_CUDA(malloc_async(&uinv, sizeof(double) * LB * LB * nblk, s));
   const int64_t tmp_elems = std::max<int64_t>({ld * LB, (int64_t)LB * (N + 1), (int64_t)LB * LB});
-  QTT_CUDA(cudaMallocAsync(&tmp, sizeof(double) * tmp_elems, s));
-  QTT_CUDA(cudaMallocAsync(&r, sizeof(double) * (N + 4), s));
-  QTT_CUDA(cudaMallocAsync(&bad, sizeof(int), s));
+  QTT_CUDA(malloc_async(&tmp, sizeof(double) * tmp_elems, s));
+  QTT_CUDA(malloc_async(&r, sizeof(double) * (N + 4), s));
+  QTT_CUDA(malloc_async(&bad, sizeof(int), s));
   nrm = r + N;
   QTT_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
   QTT_TRY(copy_matrix(s, N, N, M, ldm, A, ld));
@@ -318,8 +318,8 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
   }
   cudaStream_t sb = side_stream();
   double *Lp, *Up;
-  QTT_CUDA(cudaMallocAsync(&Lp, sizeof(double) * ld * LB, s));
-  QTT_CUDA(cudaMallocAsync(&Up, sizeof(double) * (int64_t)LB * (N + 1), s));
+  QTT_CUDA(malloc_async(&Lp, sizeof(double) * ld * LB, s));
+  QTT_CUDA(malloc_async(&Up, sizeof(double) * (int64_t)LB * (N + 1), s));
   QTT_TRY(launch_lu_diag(s, std::min(LB, N), A, ld, linv, uinv, bad));
   // Two-level blocking for large N: block pairs (a, b) share ONE trailing
   // update with K = 128 (a's update of the rows below b is deferred to b),
@@ -453,8 +453,8 @@ int dense_solve(cudaStream_t s, int N, const double* M, int64_t ldm, const doubl
   if (!ok) {
     // Householder QR: M = Q R, x = R^{-1} Q^T b (back substitution as above).
     double *Q, *R;
-    QTT_CUDA(cudaMallocAsync(&Q, sizeof(double) * ld * N, s));
-    QTT_CUDA(cudaMallocAsync(&R, sizeof(double) * ld * N, s));
+    QTT_CUDA(malloc_async(&Q, sizeof(double) * ld * N, s));
+    QTT_CUDA(malloc_async(&R, sizeof(double) * ld * N, s));
     QTT_TRY(qr(s, N, N, M, ldm, Q, ld, R, ld));
     QTT_TRY(dgemm(s, 1, 0, N, 1, N, 1.0, Q, ld, b, N, 0.0, y, N));
     for (int blk = nblk - 1; blk >= 0; --blk) {

@@ -32,7 +32,7 @@ struct DevBuf {
     if (p) cudaFreeAsync(p, s);
     p = nullptr;
     s = st;
-    QTT_CUDA(cudaMallocAsync(&p, sizeof(double) * std::max<int64_t>(n, 1), st));
+    QTT_CUDA(malloc_async(&p, sizeof(double) * std::max<int64_t>(n, 1), st));
     return kOk;
   }
   ~DevBuf() {

@@ -274,8 +274,8 @@ int gram_dot(const qtt_layout* LA, const double* a, const qtt_layout* LB, const 
   for (int l = 0; l < d; ++l)
     maxtmp = std::max(maxtmp, LA->ranks[l] * merged_n(LB, l) * LB->ranks[l + 1]);
   double *G = nullptr, *T = nullptr;
-  QTT_CUDA(cudaMallocAsync(&G, sizeof(double) * (maxr + 1), s));
-  QTT_CUDA(cudaMallocAsync(&T, sizeof(double) * maxtmp, s));
+  QTT_CUDA(malloc_async(&G, sizeof(double) * (maxr + 1), s));
+  QTT_CUDA(malloc_async(&T, sizeof(double) * maxtmp, s));
   QTT_TRY(fill(s, G, 1, 1.0));
   for (int l = 0; l < d; ++l) {
     const int ra0 = (int)LA->ranks[l], ra1 = (int)LA->ranks[l + 1];

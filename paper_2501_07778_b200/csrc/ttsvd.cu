@@ -848,11 +848,11 @@ int ttsvd_fast(cudaStream_t s, const double* dense, int d, const int64_t* sizes,
   for (int l = d - 1; l >= 0; --l) P.rest[l] = P.rest[l + 1] * sizes[l];
   P.input = dense;
   // carry buffers: every projected carry has at most `total` entries
-  QTT_CUDA(cudaMallocAsync(&res.owned[0], sizeof(double) * total, s));
-  QTT_CUDA(cudaMallocAsync(&res.owned[1], sizeof(double) * total, s));
+  QTT_CUDA(malloc_async(&res.owned[0], sizeof(double) * total, s));
+  QTT_CUDA(malloc_async(&res.owned[1], sizeof(double) * total, s));
   const size_t small = (size_t)grid * SV_NE * 2 + SV_PMAX * SV_PMAX + (size_t)d * SV_CORE;
-  QTT_CUDA(cudaMallocAsync(&res.owned[2], sizeof(double) * small, s));
-  QTT_CUDA(cudaMallocAsync(&res.owned[3], sizeof(SvState), s));
+  QTT_CUDA(malloc_async(&res.owned[2], sizeof(double) * small, s));
+  QTT_CUDA(malloc_async(&res.owned[3], sizeof(SvState), s));
   P.buf[0] = res.owned[0];
   P.buf[1] = res.owned[1];
   P.partials = res.owned[2];
@@ -923,7 +923,7 @@ int ttsvd_pack(cudaStream_t s, int d, const double* stage, const qtt_layout* out
     hv[d + l] = out->ranks[l] * out->rows[l] * out->ranks[l + 1];
   }
   int64_t* dv = nullptr;
-  QTT_CUDA(cudaMallocAsync(&dv, sizeof(int64_t) * 2 * d, s));
+  QTT_CUDA(malloc_async(&dv, sizeof(int64_t) * 2 * d, s));
   QTT_CUDA(cudaMemcpyAsync(dv, hv.data(), sizeof(int64_t) * 2 * d, cudaMemcpyHostToDevice, s));
   ttsvd_pack_kernel<<<dim3(8, std::min(d, 64)), 256, 0, s>>>(d, stage, dv, dv + d, out_data);
   QTT_CHECK_LAUNCH();
