@@ -456,29 +456,25 @@ int round_tt(const qtt_layout* in, const double* in_data, double eps, qtt_layout
   // Speculate "every small factor is well conditioned" (true for products of
   // random / full-rank TTs such as BASELINE configs 2 and 3).
   static const bool spec_on = getenv("QTT_ROUND_NO_SPEC") == nullptr;
-  thread_local int cooldown = 0;
   bool done = false, careful = false;
   if (d == 1) {
     QTT_TRY(sink.emit(s, 0, r[0] * n[0] * r[1], work.p + off[0]));
     done = true;
-  } else if (spec_on && cooldown == 0) {
+  } else if (spec_on) {
     int failed = 0;
     QTT_TRY(round_slots(s, d, r, n, off, work.p, eps, &failed, false, &sink));
     if (!failed) {
       done = true;
     } else {
       // rank-deficient or ill-conditioned small cores (sums of TT terms in
-      // assembly / coupling / the solver): this thread's next 16 roundings
-      // go straight to the Householder path
-      cooldown = 16;
+      // assembly / coupling / the solver): redo on the Householder path.  The
+      // decision depends on this call's input only (no history), so a
+      // rounding gives the same bits whenever and on whichever thread it runs.
       careful = true;
       for (int k = 0; k <= d; ++k) r[k] = in->ranks[k];
       QTT_CUDA(cudaMemcpyAsync(work.p, in_data, sizeof(double) * total, cudaMemcpyDeviceToDevice, s));
       sink.reset(d);
     }
-  } else if (cooldown > 0) {
-    --cooldown;
-    careful = true;
   }
   if (!done) QTT_TRY(round_slots(s, d, r, n, off, work.p, eps, nullptr, careful, &sink));
   *out = *in;

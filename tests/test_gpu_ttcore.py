@@ -252,7 +252,7 @@ def test_round_speculation_recovers(where):
     an exactly rank-deficient bond in the middle / near the end of the sweep.
     The sticky device flag must send the rounding back to the examined path
     and the result must match the oracle's ranks and values; repeated calls
-    (speculation cool-down of the calling thread) give the same answer."""
+    give the same bits (the path depends on the input alone)."""
     T = _T()
     d, r = 14, 64
     rng = np.random.default_rng({"middle": 11, "late": 12, "none": 13}[where])
@@ -268,11 +268,16 @@ def test_round_speculation_recovers(where):
         assert want[bond] == 20
     t = T.TTVector(cores)
     full = O.full(cores)
+    first = None
     for rep in range(3):
         got = T.tt_round(t, 1e-10)
         assert got.ranks == want, (rep, got.ranks, want)
         err = np.linalg.norm(dense_of(got) - full) / np.linalg.norm(full)
         assert err <= 1e-10 * (1 + 1e-8) + 1e-13
+        if first is None:
+            first = got.numpy_cores()
+        else:
+            assert all(np.array_equal(a, b) for a, b in zip(first, got.numpy_cores()))
 
 
 @pytest.mark.parametrize("case", ["full", "truncating", "deficient"])
@@ -306,11 +311,12 @@ def test_round_streams_cores_to_host(case):
         for a, c in zip(hst.cores, hst.numpy_cores()):
             assert isinstance(a, np.ndarray) and not a.flags.writeable
             assert np.array_equal(a, c)
-        # (two separate roundings may differ in gauge: the calling thread's
-        # speculation cool-down picks CholeskyQR2 or Householder factors)
+        # and equal to a separate rounding of the same input (the path depends
+        # on the input alone)
+        for a, b in zip(hst.cores, dev.numpy_cores()):
+            assert np.array_equal(a, b)
         got = O.full([np.array(a) for a in hst.cores])
         assert np.linalg.norm(got - full) <= 1e-9 * (1 + 1e-6) * np.linalg.norm(full)
-        assert np.linalg.norm(got - dense_of(dev)) <= 1e-12 * np.linalg.norm(full)
 
 
 def test_round_matrix():
