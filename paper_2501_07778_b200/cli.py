@@ -5,6 +5,7 @@ through the device pipeline and emits the SPEC's CSV rows.
     python -m paper_2501_07778_b200.cli run   --case config4 --d 8 --eps 1e-8 --out row.csv
     python -m paper_2501_07778_b200.cli sweep --case config1 --d 3 4 5 --eps 1e-6 1e-8 --out sweep.csv
     python -m paper_2501_07778_b200.cli report sweep.csv
+    python -m paper_2501_07778_b200.cli verify --case config5 --d 4
 
 Cases are the BASELINE.json geometries (config1, config4, config4_constE,
 config5).  ``l2_error`` is the relative error against the committed
@@ -78,6 +79,44 @@ def run_case(case: str, d: int, eps: float, seed: int = 0, save_u: str | None = 
                        storage_f=pf.storage_count, wall_ms=wall_ms, converged=bool(res.converged))
 
 
+def verify_case(case: str, d: int, eps: float = 1e-8) -> list:
+    """SPEC.md:579-586 ``verify`` (d <= 4): dense-equality and
+    conforming-equivalence properties of the device pipeline.  Returns a list
+    of (property, value, bound, ok)."""
+    import numpy as np
+
+    from . import solver as S
+    from . import ttcore as T
+    from .configs import build_system
+
+    if d > 4:
+        raise ValueError("verify needs d <= 4 (dense comparisons)")
+    idx = CASES[case]
+    gsys, _ = build_system(idx, d)
+    res = S.solve(gsys.K, gsys.f, S.SolverConfig(epsilon=eps, seed=0, local_solver="direct"))
+    Kd = T.tt_contract(gsys.K)
+    fd = T.tt_contract(gsys.f)
+    ud = T.tt_contract(res.u)
+    checks = []
+    if idx != 5:  # the penalty-coupled multi-patch operator is not symmetric (coupling.py:333-485)
+        sym = float(np.abs(Kd - Kd.T).max() / np.abs(Kd).max())
+        checks.append(("K symmetric (dense)", sym, 1e-10, sym <= 1e-10))
+    r_dense = float(np.linalg.norm(Kd @ ud - fd) / np.linalg.norm(fd))
+    checks.append(("dense residual ||K u - f|| / ||f||", r_dense, eps, r_dense <= eps))
+    u_exact = np.linalg.solve(Kd, fd)
+    e_dense = float(np.linalg.norm(ud - u_exact) / np.linalg.norm(u_exact))
+    bound = 10 * eps * float(np.linalg.cond(Kd))
+    checks.append(("u vs dense solve", e_dense, bound, e_dense <= bound))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    fx = os.path.join(root, "tests", "golden", f"conforming_c{idx}_d{d}.npz")
+    if os.path.exists(fx):
+        c = np.load(fx)
+        uc = T.tt_contract(T.TTVector([c[f"cores_{k}"] for k in range(len(c["ranks"]) - 1)]))
+        e_conf = float(np.linalg.norm(ud - uc) / np.linalg.norm(uc))
+        checks.append(("u vs conforming FEM (splu fixture)", e_conf, 1e-6, e_conf <= 1e-6))
+    return checks
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="paper_2501_07778_b200.cli", description=__doc__,
                                  formatter_class=argparse.RawDescriptionHelpFormatter)
@@ -92,7 +131,17 @@ def main(argv=None) -> int:
         p.add_argument("--save-u", default=None)
     p = sub.add_parser("report")
     p.add_argument("csv")
+    p = sub.add_parser("verify")
+    p.add_argument("--case", choices=sorted(CASES), required=True)
+    p.add_argument("--d", type=int, required=True)
     a = ap.parse_args(argv)
+    if a.cmd == "verify":
+        if not 2 <= a.d <= 4:
+            ap.error("verify takes d in [2, 4]")
+        checks = verify_case(a.case, a.d)
+        for name, val, bound, ok in checks:
+            print(f"{'pass' if ok else 'FAIL'}  {name}: {val:.3e} (bound {bound:.1e})")
+        return 0 if all(c[3] for c in checks) else 1
     if a.cmd == "report":
         for r in read_csv(a.csv):
             print(f"{r.case:>16} d={r.d:<2} eps={r.eps:g} dofs={r.dofs} R_d={r.Rd} N_d={r.Nd} "

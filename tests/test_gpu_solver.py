@@ -251,3 +251,13 @@ def test_cli_run_and_snapshot(tmp_path):
     assert row.l2_error < 1e-8  # against tests/golden/conforming_c1_d4.npz
     u = ttio.load_tt(str(snap))
     assert max(u.ranks) == row.Rd and T.rank_profile(u).param_count == row.Nd
+
+
+@pytest.mark.parametrize("case,d", [("config1", 4), ("config4", 4), ("config5", 4)])
+def test_cli_verify(case, d):
+    """bench_cli verify: dense-equality and conforming-equivalence at d = 4."""
+    from paper_2501_07778_b200 import cli
+
+    checks = cli.verify_case(case, d)
+    assert len(checks) == (3 if case == "config5" else 4), checks  # conforming fixtures exist for these cases
+    assert all(ok for _, _, _, ok in checks), checks
