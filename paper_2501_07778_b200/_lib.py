@@ -186,7 +186,7 @@ _STREAMS: list = []
 class _Worker:
     """One host thread bound to one chain slot: slot i always runs on thread i
     with stream i, so the library's per-thread state (private memory pool,
-    look-ahead side stream, speculation cool-down) stays with the chain."""
+    look-ahead side stream) stays with the chain."""
 
     def __init__(self, idx: int):
         import queue

@@ -460,6 +460,51 @@ __global__ void __launch_bounds__(256) cert_small_kernel(int k, const double* __
   }
 }
 
+// The same certificate for k <= 32 by ONE warp: lane l back-substitutes column
+// l of R^{-1} out of registers (the small bonds at both ends of every TT).
+__global__ void __launch_bounds__(32) cert_tiny_kernel(int k, const double* __restrict__ R, int64_t ldr,
+                                                       const double* delta_dev, double delta_scale,
+                                                       int* ok_dev, int* sflag, int debug) {
+  __shared__ double S[32][33];
+  const int l = threadIdx.x;
+  double rn = 0.0;
+#pragma unroll 8
+  for (int i = 0; i < 32; ++i) {
+    double v = (i == l) ? 1.0 : 0.0;
+    if (i < k && l < k) v = (i <= l) ? R[i + (int64_t)l * ldr] : 0.0;
+    S[i][l] = v;
+    if (i < k && l < k) rn = fma(v, v, rn);
+  }
+  __syncwarp();
+  double v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = 0.0;
+#pragma unroll
+  for (int k2 = 31; k2 >= 0; --k2) {
+    const double dinv = 1.0 / S[k2][k2];
+    const double xk = (l == k2) ? dinv : (l > k2 ? -v[k2] * dinv : 0.0);
+    v[k2] = xk;
+#pragma unroll
+    for (int i = 0; i < k2; ++i) v[i] = fma(S[i][k2], xk, v[i]);
+  }
+  double xn = 0.0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < k && l < k) xn = fma(v[i], v[i], xn);
+  rn = sqrt(warp_sum(rn));
+  xn = sqrt(warp_sum(xn));
+  if (l == 0) {
+    const double eps = 2.220446049250313e-16;
+    const double delta = delta_dev ? (*delta_dev) * delta_scale : 0.0;
+    const double thr = fmax(delta, rn * (double)max(k, 2) * eps);
+    const bool good = isfinite(xn) && isfinite(rn) && xn > 0.0 && (1.0 / xn) > 1.25 * thr;
+    if (ok_dev) *ok_dev = good ? 1 : 0;
+    if (sflag && !good) atomicOr(sflag, 2);
+    if (debug) printf("[cert-tiny] k=%d smin/||R||>=%.3e thr/||R||=%.3e good=%d\n", k, 1.0 / xn / rn,
+                      thr / rn, (int)good);
+  }
+}
+
 // ------------------------------------------------ small fused factor, v2
 // Same contract as chol_inv_small_kernel, organised for latency: blocks of
 // 32, the matrix in shared memory (row stride 129), and each 32 x 32 diagonal
@@ -886,6 +931,11 @@ int cert_small(cudaStream_t s, int k, const double* R, int64_t ldr, const double
     configured.set();
   }
   static const int debug = getenv("QTT_CERT_DEBUG") ? 1 : 0;
+  if (k <= 32) {
+    cert_tiny_kernel<<<1, 32, 0, s>>>(k, R, ldr, delta_dev, delta_scale, ok_dev, sflag, debug);
+    QTT_CHECK_LAUNCH();
+    return kOk;
+  }
   cert_small_kernel<<<1, 256, kCisSmem, s>>>(k, R, ldr, delta_dev, delta_scale, ok_dev, sflag, debug);
   QTT_CHECK_LAUNCH();
   return kOk;

@@ -220,8 +220,8 @@ int qr_cert_spec(cudaStream_t s, int m, int n, const double* A, int64_t lda, dou
 int round_slots(cudaStream_t s, int d, std::vector<int64_t>& r, const std::vector<int64_t>& n,
                 const std::vector<int64_t>& off, double* work, double eps, int* spec_failed,
                 bool careful, CoreSink* sink) {
-  // careful: skip the CholeskyQR2 attempt for small factors (a thread whose
-  // recent roundings met rank-deficient cores goes straight to Householder)
+  // careful: skip the CholeskyQR2 attempt for small factors (the rerun after a
+  // failed speculation goes straight to Householder)
   if (spec_failed) *spec_failed = 0;
   if (d == 1) return kOk;
   int64_t maxcore = 1;
